@@ -1,0 +1,183 @@
+"""Pins for oracle.projector / oracle.spectrum — Table 3 Steps 3-4 and
+Table 2 Step-5 on the ULA grid (EV weighting Q1; MN normalisation Q5).
+
+Pins: projector invariants (MUSIC idempotent with trace M-D; PHD/MN rank one; MN w_0 = 1;
+EV with a flat noise floor = MUSIC / sigma^2), LAPACK-built projectors, the V = I injection
+(constant spectra), whole-spectrum closed forms for a noise-free single source (MUSIC and MN),
+the exact null at the true angle, a 50-digit mpmath evaluation of a^H C a, the d = lambda/2
+endpoint identity, the count of interior minima of a degree-(M-1) trigonometric polynomial,
+and thread-count invariance.
+"""
+import mpmath as mp
+import numpy as np
+import pytest
+
+from synth import get_config, generate
+
+EPS = np.finfo(float).eps
+ALGS = ["phd", "music", "ev", "mn"]
+
+
+def _grid_u(theta0, dtheta, L, dl=0.5):
+    th = theta0 + np.arange(L) * dtheta
+    return 2 * dl * np.sin(np.deg2rad(th))
+
+
+def _noisy_R(orc, cfg, frame=0):
+    return orc.covariance(generate(cfg, frames=[frame])[0])
+
+
+def test_projector_invariants(orc):
+    cfg = get_config("c2")
+    R = _noisy_R(orc, cfg)
+    lam, V, _, _ = orc.eig(R)
+    M, D = cfg.M, cfg.D
+    Cmu, _ = orc.projector("music", D, lam, V)
+    assert np.linalg.norm(Cmu @ Cmu - Cmu) <= 1e-13
+    assert abs(np.trace(Cmu).real - (M - D)) <= 1e-13
+    assert np.linalg.norm(Cmu - Cmu.conj().T) <= 1e-14
+    # MUSIC C = I - E_s E_s^H with E_s from LAPACK
+    w, U = np.linalg.eigh(R)
+    Es = U[:, M - D:]
+    assert np.linalg.norm(Cmu - (np.eye(M) - Es @ Es.conj().T)) <= 1e-12
+    for alg in ("phd", "mn"):
+        Cx, _ = orc.projector(alg, D, lam, V)
+        s = np.linalg.svd(Cx, compute_uv=False)
+        assert s[1] <= 1e-14 * s[0], alg        # rank one
+    Cmn, _ = orc.projector("mn", D, lam, V)
+    assert abs(Cmn[0, 0] - 1.0) <= 1e-13       # w_0 = 1 (lambda' = (e1^H P_n e1)^-1)
+    # MN from LAPACK's noise projector: valph = P_n e1 / (e1^H P_n e1)
+    Pn = U[:, : M - D] @ U[:, : M - D].conj().T
+    v = Pn[:, 0] / Pn[0, 0].real
+    assert np.linalg.norm(Cmn - np.outer(v, v.conj())) <= 1e-11
+    # EV = sum_k (1/lambda_k) e_k e_k^H with LAPACK's pairs
+    Cev, _ = orc.projector("ev", D, lam, V)
+    ref = (U[:, : M - D] / w[: M - D]) @ U[:, : M - D].conj().T
+    assert np.linalg.norm(Cev - ref) <= 1e-11 * np.linalg.norm(ref)
+    # PHD = e_min e_min^H
+    Cp, _ = orc.projector("phd", D, lam, V)
+    assert np.linalg.norm(Cp - np.outer(U[:, 0], U[:, 0].conj())) <= 1e-11
+
+
+def test_ev_flat_noise_floor_equals_music_over_sigma2(orc):
+    M, D, sig2 = 12, 2, 0.25
+    m = np.arange(M)
+    R = sig2 * np.eye(M, dtype=complex)
+    for k in (1, 7):  # DFT-orthogonal sources: noise eigenvalues exactly sigma^2 up to rounding
+        a = np.exp(-1j * np.pi * m * (-1 + 2 * k / M))
+        R += np.outer(a, a.conj())
+    lam, V, _, _ = orc.eig(R)
+    Cev, _ = orc.projector("ev", D, lam, V)
+    Cmu, _ = orc.projector("music", D, lam, V)
+    assert np.linalg.norm(Cev - Cmu / sig2) <= 1e-12 / sig2
+
+
+def test_identity_injection_constant_spectra(orc):
+    # V = I: PHD f = |a_0|^2 = 1, MN f = |a_0|^2 = 1 exactly; MUSIC f = M - D, EV f = sum 1/lambda_k
+    M, D, L = 16, 3, 1801
+    lam = np.linspace(0.5, 4.0, M)
+    V = np.eye(M, dtype=complex)
+    for alg in ALGS:
+        f, info = orc.spectrum(alg, D, 0.5, lam, V, -90.0, 0.1, L)
+        ref = {"phd": 1.0, "mn": 1.0, "music": M - D, "ev": np.sum(1 / lam[: M - D])}[alg]
+        assert np.max(np.abs(f - ref)) <= 4 * M * EPS * ref, alg
+        if alg in ("phd", "mn"):
+            assert np.all(f == 1.0)
+            assert orc.peaks(f, D)[2] == 0          # constant spectrum: no peaks
+
+
+@pytest.mark.parametrize("M,th0", [(8, 23.0), (16, -41.3), (16, 10.0), (64, 12.5)])
+def test_noise_free_single_source_closed_forms(orc, M, th0):
+    # R = a0 a0^H: MUSIC f = M - sin^2(M D/2) / (M sin^2(D/2)), D = pi (u - u0);
+    # MN |w^H a|^2 = |1 - (1/M) sum_m e^{-j pi m (u - u0)}|^2 / (1 - 1/M)^2.
+    m = np.arange(M)
+    u0 = np.sin(np.deg2rad(th0))
+    a0 = np.exp(-1j * np.pi * m * u0)
+    R = np.outer(a0, a0.conj())
+    lam, V, _, _ = orc.eig(R)
+    L, dth = 3601, 0.05
+    u = _grid_u(-90.0, dth, L)
+    Dl = np.pi * (u - u0)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        fej = np.where(np.abs(np.sin(Dl / 2)) < 1e-300, M,
+                       np.sin(M * Dl / 2) ** 2 / (M * np.sin(Dl / 2) ** 2))
+    f_mu, _ = orc.spectrum("music", 1, 0.5, lam, V, -90.0, dth, L)
+    np.testing.assert_allclose(f_mu, np.maximum(M - fej, 1e-300), rtol=0, atol=1e-12 * M)
+    s = np.exp(-1j * np.pi * np.outer(u - u0, m)).sum(axis=1) / M
+    ref_mn = np.abs(1 - s) ** 2 / (1 - 1 / M) ** 2
+    f_mn, _ = orc.spectrum("mn", 1, 0.5, lam, V, -90.0, dth, L)
+    np.testing.assert_allclose(f_mn, np.maximum(ref_mn, 1e-300), rtol=0, atol=1e-11)
+
+
+@pytest.mark.parametrize("alg", ["phd", "music", "mn", "ev"])
+def test_exact_null_at_true_on_grid_angle(orc, alg):
+    # north_star: "noise-free single source gives an exact null at the true theta" -> the
+    # top-1 peak index is the true grid index.
+    M, dth = 16, 0.01
+    i_true = 13421
+    th0 = -90.0 + i_true * dth
+    m = np.arange(M)
+    a0 = np.exp(-1j * np.pi * m * np.sin(th0 * np.pi / 180))
+    R = np.outer(a0, a0.conj()) + 1e-3 * np.eye(M)      # sigma^2 > 0 keeps EV finite
+    lam, V, _, _ = orc.eig(R)
+    f, _ = orc.spectrum(alg, 1, 0.5, lam, V, -90.0, dth, 18001)
+    idx, fv, npk, _ = orc.peaks(f, 1)
+    assert npk == 1 and idx[0] == i_true
+    assert fv[0] <= 1e-20 * np.max(f)
+
+
+def test_sum_of_squares_equals_aHCa_and_mpmath(orc):
+    cfg = get_config("c2")
+    R = _noisy_R(orc, cfg)
+    lam, V, _, _ = orc.eig(R)
+    L, dth = 1801, 0.1
+    u = _grid_u(-90.0, dth, L)
+    M = cfg.M
+    A = np.exp(-1j * np.pi * np.outer(np.arange(M), u))        # (M, L)
+    mp.mp.dps = 40
+    pick = [3, 200, 555, 901, 1200, 1799]
+    for alg in ALGS:
+        f, _ = orc.spectrum(alg, cfg.D, 0.5, lam, V, -90.0, dth, L)
+        Cm, _ = orc.projector(alg, cfg.D, lam, V)
+        q = np.einsum("ml,mn,nl->l", A.conj(), Cm, A).real
+        scale = np.sum(np.abs(Cm)) * M
+        assert np.max(np.abs(f - q)) <= 1e3 * EPS * scale, alg
+        Cmp = mp.matrix([[mp.mpc(Cm[i, j].real, Cm[i, j].imag) for j in range(M)] for i in range(M)])
+        for i in pick:
+            th = mp.mpf(-90) + i * mp.mpf(dth)
+            uu = mp.sin(th * mp.pi / 180)
+            a = mp.matrix([mp.expj(-mp.pi * mm * uu) for mm in range(M)])
+            ref = (a.H * Cmp * a)[0].real
+            assert abs(float(ref) - f[i]) <= 1e-13 * scale, (alg, i)
+
+
+def test_endpoint_symmetry_and_interior_minima(orc):
+    cfg = get_config("c4")
+    X = generate(cfg, frames=range(4))
+    for b in range(4):
+        lam, V, _, _ = orc.eig(orc.covariance(X[b]))
+        for alg in ALGS:
+            f, _ = orc.spectrum(alg, cfg.D, 0.5, lam, V, -90.0, 0.01, 18001)
+            assert abs(f[0] - f[-1]) <= 1e-12 * max(f[0], f[-1])      # a(-90) = a(+90) at d = lambda/2
+            assert np.all(f > 0)
+            n = orc.peaks(f, cfg.D)[3]
+            assert n <= cfg.M - 1                                       # degree M-1 trig polynomial
+
+
+def test_thread_count_invariance(orc):
+    cfg = get_config("c2")
+    lam, V, _, _ = orc.eig(_noisy_R(orc, cfg))
+    for alg in ALGS:
+        f1, _ = orc.spectrum(alg, cfg.D, 0.5, lam, V, -90.0, 0.01, 18001, threads=1)
+        f4, _ = orc.spectrum(alg, cfg.D, 0.5, lam, V, -90.0, 0.01, 18001, threads=5)
+        assert np.array_equal(f1, f4)
+
+
+def test_ev_degenerate_flag(orc):
+    M = 8
+    m = np.arange(M)
+    a0 = np.exp(-1j * np.pi * m * 0.3)
+    lam, V, _, _ = orc.eig(np.outer(a0, a0.conj()))       # noise eigenvalues ~ 0
+    f, info = orc.spectrum("ev", 1, 0.5, lam, V, -90.0, 1.0, 181)
+    assert info & orc.INFO_DEGENERATE
+    assert np.all(np.isfinite(f))
