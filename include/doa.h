@@ -1,0 +1,152 @@
+/*
+ * doa.h — C ABI of the B200-native noise-subspace DOA hot path (libdoa.so).
+ *
+ * Method: Eray & Temizel, arXiv 2007.14135, "Performance Analysis of Noise Subspace-based
+ * Narrowband DOA Estimation Algorithms on CPU and GPU".  Citations "P:n" are lines of the
+ * paper text; "Qn" are the readings of silent/ambiguous points listed in
+ * DESIGN.md §2.
+ *
+ * Problem statement: an M-element uniform linear array with
+ * spacing d (ratio d/lambda), D known narrowband sources, N snapshots X per frame and a scan
+ * grid theta_i = theta0 + i*dtheta (degrees from broadside, i in [0, L)).  Per frame return the
+ * pseudo-spectrum P(theta_i) = 1 / (a(theta_i)^H C a(theta_i)) of one of PHD / MUSIC / EV / MN
+ * and its D strongest local maxima (the DOA estimates), with the steering vector
+ * a_m(theta) = exp(-j*2*pi*(d/lambda)*m*sin(theta)), m = 0..M-1 (Q6).
+ *
+ * Conventions shared by every call
+ *  - Every data pointer is a DEVICE pointer owned by the caller (e.g. a torch CUDA tensor),
+ *    except in doa_run_host, whose X/outputs are HOST pointers.  Complex numbers are
+ *    interleaved (re, im): complex64 = 2 x float (8-byte aligned), complex128 = 2 x double
+ *    (16-byte aligned).  All arrays are dense row-major.
+ *  - Calls are asynchronous: they validate their arguments on the host, enqueue kernels on
+ *    `stream` and return.  Only doa_plan_create / doa_plan_destroy / doa_run_host synchronise.
+ *  - Invalid arguments return DOA_ERR_INVALID_ARG (or DOA_ERR_UNSUPPORTED) synchronously and
+ *    enqueue nothing.  A CUDA launch / allocation failure returns DOA_ERR_CUDA /
+ *    DOA_ERR_OUT_OF_MEMORY; doa_last_error() gives the detail (thread-local).
+ *  - B == 0 is valid and enqueues nothing.
+ *  - Per-frame numerical conditions never fail a call; they set bits of the caller's
+ *    info[b] (DOA_INFO_*): doa_eig overwrites info[b]; doa_spectrum and doa_peaks OR into it.
+ *  - A plan owns only its workspace (candidate lists and, for doa_run, R / lambda / V /
+ *    coefficient scratch for max_batch frames).  One plan must not be used from two streams
+ *    at once; doa_peaks consumes the candidates written by the preceding doa_spectrum on the
+ *    same plan, in stream order.
+ *  - Arithmetic: fp32 inputs, fp64 everywhere inside; P and peak values are
+ *    reported in fp32, saturating at FLT_MAX (Q12).
+ */
+#ifndef DOA_H_
+#define DOA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct doa_plan_s* doa_plan_t;
+typedef struct CUstream_st* doa_stream_t;   /* == cudaStream_t; NULL = legacy default stream */
+
+/* Table 3: the four noise-subspace estimators. */
+typedef enum {
+  DOA_ALG_PHD = 0,    /* C = e_min e_min^H                         (Table 3) */
+  DOA_ALG_MUSIC = 1,  /* C = E_n E_n^H          */
+  DOA_ALG_EV = 2,     /* C = sum_k (1/lambda_k) e_k e_k^H  (Q1)          */
+  DOA_ALG_MN = 3      /* C = w w^H, w = P_n e1 / (e1^H P_n e1)     (Q5)      */
+} doa_alg_t;
+
+typedef enum {
+  DOA_OK = 0,
+  DOA_ERR_INVALID_ARG = 1,
+  DOA_ERR_UNSUPPORTED = 2,
+  DOA_ERR_OUT_OF_MEMORY = 3,
+  DOA_ERR_CUDA = 4
+} doa_status_t;
+
+enum {
+  DOA_INFO_NOCONV = 1,          /* Jacobi hit 30 sweeps; outputs are the last iterate (Q15)     */
+  DOA_INFO_DEGENERATE = 2,      /* EV noise eigenvalue <= 100 eps lambda_max (clamped), or MN
+                                   e1^H P_n e1 <= 100 eps (w = P_n e1 unnormalised)             */
+  DOA_INFO_CAND_OVERFLOW = 4,   /* more local maxima than the plan's candidate capacity; the
+                                   peaks are chosen from the first `capacity` found             */
+  DOA_INFO_UNDERDETERMINED = 8  /* fewer than D local maxima (npk < D; padding -1 / 0)          */
+};
+
+/* Create a plan.  M in [2, 64] (M > 64: DOA_ERR_UNSUPPORTED); 1 <= D < M; d_over_lambda > 0;
+ * grid theta_i = theta0_deg + i*dtheta_deg (multiply then add, round-to-nearest; Q8) for i in
+ * [0, L), 3 <= L < 2^31, dtheta_deg > 0, theta0_deg >= -90, theta0_deg + (L-1)*dtheta_deg <=
+ * 90 (+1e-9); alg a doa_alg_t; max_batch >= 1 frames per call.  Allocates the workspace
+ * (synchronous).  On failure *plan is set to NULL. */
+doa_status_t doa_plan_create(doa_plan_t* plan, int32_t M, double d_over_lambda, int32_t D,
+                             double theta0_deg, double dtheta_deg, int64_t L, int32_t alg,
+                             int64_t max_batch);
+
+/* Free the plan and its workspace (synchronises the device).  NULL is a no-op. */
+doa_status_t doa_plan_destroy(doa_plan_t plan);
+
+/* Number of candidate slots per frame the plan reserves (>= 2*((M-1)*ceil(2 d/lambda)+1)). */
+int32_t doa_plan_capacity(doa_plan_t plan);
+
+/* S1 — sample covariance, Eq. 3 / Table 2 Step-1:
+ *   R[b] = (1/N) sum_n x_b[n] x_b[n]^H   (1/N, Q20).
+ * X: complex64 [B][N][M] (snapshot-major: x_m[n] of frame b at X[(b*N+n)*M+m]).
+ * R: complex128 [B][M][M], full Hermitian, real diagonal.  fp32 products are exact in fp64;
+ * sums are accumulated in fp64 in a fixed order (deterministic).  N >= 1, 1 <= B <= max_batch. */
+doa_status_t doa_covariance(doa_plan_t plan, const float* X, int64_t B, int64_t N, double* R,
+                            doa_stream_t stream);
+
+/* S2 — Hermitian eigendecomposition of R (Table 2 Step-2 `jsvd`; Q3), one warp per matrix,
+ * parallel (round-robin) cyclic Jacobi in fp64.  Only the upper triangle of R[b] is read.
+ * Stop when off(A) <= 10 eps ||R||_F (off computed directly), at most 30 sweeps (Q15).
+ * lambda: double [B][M] ascending (stable, Q2).  V: complex128 [B][M][M], column j (V[b][i][j],
+ * i = 0..M-1) is the unit eigenvector of lambda[b][j].  info[b] is OVERWRITTEN (NOCONV or 0). */
+doa_status_t doa_eig(doa_plan_t plan, const double* R, int64_t B, double* lambda, double* V,
+                     int32_t* info, doa_stream_t stream);
+
+/* S3-S6 — noise subspace (Table 3 Step-3), Step-4 form C reduced to its Toeplitz diagonal sums
+ * c_k = sum_p C[p][p+k], pseudo-spectrum scan over the plan's grid
+ * (Table 2 Step-5) f_i = a_i^H C a_i = c_0 + 2 sum_k Re(c_k e^{-j pi k u_i}),
+ * u_i = 2 (d/lambda) sin(theta_i), floored at 1e-300 (Q12), and local-maximum candidate
+ * detection (Step-6 findPeaks; Q9/Q10) into the plan's candidate lists.
+ * lambda/V as produced by doa_eig.  P: NULL, or float [B][L] receiving 1/f_i (fp32, saturating).
+ * info[b] |= DEGENERATE where applicable. */
+doa_status_t doa_spectrum(doa_plan_t plan, const double* lambda, const double* V, int64_t B,
+                          float* P, int32_t* info, doa_stream_t stream);
+
+/* S7 — PeakSelection (Table 2 Step-6; Q11): per frame order the plan's candidates by
+ * (f ascending, index ascending) and keep min(D, count).  idx: int32 [B][D] grid indices (-1
+ * padding), val: float [B][D] = 1/f (0 padding), npk: int32 [B].  info[b] |= CAND_OVERFLOW,
+ * UNDERDETERMINED.  B must equal the preceding doa_spectrum's B. */
+doa_status_t doa_peaks(doa_plan_t plan, int64_t B, int32_t* idx, float* val, int32_t* npk,
+                       int32_t* info, doa_stream_t stream);
+
+/* S1-S7 fused: X (device, as doa_covariance) -> idx/val/npk/info (device, as doa_peaks),
+ * P nullable (as doa_spectrum).  info[b] is overwritten.  Uses plan scratch for R, lambda, V
+ * (max_batch frames), allocated by the first doa_run / doa_run_host on the plan (that first call
+ * synchronises the device once). */
+doa_status_t doa_run(doa_plan_t plan, const float* X, int64_t B, int64_t N, int32_t* idx,
+                     float* val, int32_t* npk, float* P, int32_t* info, doa_stream_t stream);
+
+/* End-to-end variant of doa_run with HOST buffers, for nplans >= 1 plans that share M and D
+ * (typically the four estimators): X_host complex64 [B][N][M] is copied host->device in chunks
+ * on a second stream into device staging owned by plans[0], overlapping each chunk's copy with
+ * the compute of the previous chunk; per chunk S1-S2 run once and S3-S7 once per plan; the
+ * peak lists come back to the host outputs idx_host int32 [nplans][B][D], val_host float
+ * [nplans][B][D], npk_host int32 [nplans][B], info_host int32 [nplans][B].  Synchronises
+ * `stream` before returning.  X_host should be pinned (page-locked) for asynchronous copies;
+ * pageable memory is accepted and copied synchronously by the driver.  The staging buffers are
+ * allocated on first use (and grown if a later call needs more). */
+doa_status_t doa_run_host(const doa_plan_t* plans, int32_t nplans, const float* X_host, int64_t B,
+                          int64_t N, int32_t* idx_host, float* val_host, int32_t* npk_host,
+                          int32_t* info_host, doa_stream_t stream);
+
+/* Kernel launches the most recent call on this thread enqueued (for launch accounting). */
+int32_t doa_last_launch_count(void);
+
+const char* doa_status_string(doa_status_t status);
+const char* doa_last_error(void);
+int32_t doa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DOA_H_ */

@@ -1,0 +1,326 @@
+// C ABI of libdoa (include/doa.h): argument validation, plan/workspace management, error
+// reporting, and the composition of the kernels into doa_run / doa_run_host.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "doa_internal.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+doa_status_t fail(doa_status_t st, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+doa_status_t fail(doa_status_t st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+doa_status_t cuda_fail(cudaError_t e, const char* where) {
+  return fail(e == cudaErrorMemoryAllocation ? DOA_ERR_OUT_OF_MEMORY : DOA_ERR_CUDA, "%s: %s (%s)", where,
+              cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+#define DOA_CHECK_PLAN(p)                                                   \
+  do {                                                                      \
+    if (!(p)) return fail(DOA_ERR_INVALID_ARG, "%s: plan is NULL", __func__); \
+  } while (0)
+#define DOA_CHECK_PTR(ptr, al)                                                                         \
+  do {                                                                                                 \
+    if (!(ptr)) return fail(DOA_ERR_INVALID_ARG, "%s: %s is NULL", __func__, #ptr);                    \
+    if (!aligned((ptr), (al))) return fail(DOA_ERR_INVALID_ARG, "%s: %s is not %d-byte aligned", __func__, #ptr, (int)(al)); \
+  } while (0)
+#define DOA_CHECK_B(p, B)                                                                                  \
+  do {                                                                                                     \
+    if ((B) < 0 || (B) > (p)->max_batch)                                                                   \
+      return fail(DOA_ERR_INVALID_ARG, "%s: B=%lld outside [0, max_batch=%lld]", __func__, (long long)(B), \
+                  (long long)(p)->max_batch);                                                              \
+  } while (0)
+#define DOA_TRY(expr, where)                       \
+  do {                                             \
+    cudaError_t e_ = (expr);                       \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+// R / lambda / V scratch for doa_run, allocated on first use.
+cudaError_t ensure_run_scratch(doa_plan_s* p) {
+  if (p->R) return cudaSuccess;
+  const size_t B = (size_t)p->max_batch, M = (size_t)p->M;
+  cudaError_t e = cudaMalloc((void**)&p->R, B * M * M * 2 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&p->lam, B * M * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&p->V, B * M * M * 2 * sizeof(double));
+  if (e != cudaSuccess) {
+    cudaFree(p->R); cudaFree(p->lam); cudaFree(p->V);
+    p->R = nullptr; p->lam = nullptr; p->V = nullptr;
+  }
+  return e;
+}
+
+}  // namespace
+
+namespace doa {
+void count_launch() { ++g_launches; }
+}  // namespace doa
+
+extern "C" {
+
+int32_t doa_version(void) { return 1; }
+int32_t doa_last_launch_count(void) { return g_launches; }
+const char* doa_last_error(void) { return g_err.c_str(); }
+
+const char* doa_status_string(doa_status_t s) {
+  switch (s) {
+    case DOA_OK: return "DOA_OK";
+    case DOA_ERR_INVALID_ARG: return "DOA_ERR_INVALID_ARG";
+    case DOA_ERR_UNSUPPORTED: return "DOA_ERR_UNSUPPORTED";
+    case DOA_ERR_OUT_OF_MEMORY: return "DOA_ERR_OUT_OF_MEMORY";
+    case DOA_ERR_CUDA: return "DOA_ERR_CUDA";
+  }
+  return "DOA_ERR_UNKNOWN";
+}
+
+doa_status_t doa_plan_create(doa_plan_t* plan, int32_t M, double d_over_lambda, int32_t D, double theta0_deg,
+                             double dtheta_deg, int64_t L, int32_t alg, int64_t max_batch) {
+  g_launches = 0;
+  if (!plan) return fail(DOA_ERR_INVALID_ARG, "doa_plan_create: plan out-pointer is NULL");
+  *plan = nullptr;
+  if (M < 2) return fail(DOA_ERR_INVALID_ARG, "doa_plan_create: M=%d < 2", M);
+  if (M > doa::kMaxM) return fail(DOA_ERR_UNSUPPORTED, "doa_plan_create: M=%d > %d", M, doa::kMaxM);
+  if (D < 1 || D >= M) return fail(DOA_ERR_INVALID_ARG, "doa_plan_create: D=%d outside [1, M-1]", D);
+  if (!(d_over_lambda > 0.0) || !std::isfinite(d_over_lambda))
+    return fail(DOA_ERR_INVALID_ARG, "doa_plan_create: d/lambda=%g must be positive and finite", d_over_lambda);
+  if (L < 3 || L >= (int64_t)1 << 31) return fail(DOA_ERR_INVALID_ARG, "doa_plan_create: L=%lld outside [3, 2^31)", (long long)L);
+  if (!(dtheta_deg > 0.0) || !std::isfinite(dtheta_deg))
+    return fail(DOA_ERR_INVALID_ARG, "doa_plan_create: dtheta=%g must be positive", dtheta_deg);
+  if (!(theta0_deg >= -90.0)) return fail(DOA_ERR_INVALID_ARG, "doa_plan_create: theta0=%g < -90", theta0_deg);
+  if (!(theta0_deg + (double)(L - 1) * dtheta_deg <= 90.0 + 1e-9))
+    return fail(DOA_ERR_INVALID_ARG, "doa_plan_create: grid end %g > 90", theta0_deg + (double)(L - 1) * dtheta_deg);
+  if (alg < DOA_ALG_PHD || alg > DOA_ALG_MN) return fail(DOA_ERR_INVALID_ARG, "doa_plan_create: alg=%d", alg);
+  if (max_batch < 1) return fail(DOA_ERR_INVALID_ARG, "doa_plan_create: max_batch=%lld < 1", (long long)max_batch);
+
+  doa_plan_s* p = new doa_plan_s();
+  std::memset(p, 0, sizeof *p);
+  p->M = M; p->D = D; p->alg = alg; p->dl = d_over_lambda; p->theta0 = theta0_deg; p->dtheta = dtheta_deg;
+  p->L = L; p->max_batch = max_batch;
+  // interior minima of a degree-(M-1) trig polynomial over ceil(2 d/lambda) periods, x2 margin, >= 32
+  int cap = 2 * ((M - 1) * (int)std::ceil(2.0 * d_over_lambda) + 1);
+  cap = (cap + 31) & ~31;
+  p->cap = cap;
+  const size_t B = (size_t)max_batch;
+  cudaError_t e = cudaSuccess;
+  auto al = [&](void** ptr, size_t bytes) { if (e == cudaSuccess) e = cudaMalloc(ptr, bytes); };
+  al((void**)&p->cnt, B * sizeof(int32_t));
+  al((void**)&p->cand_idx, B * cap * sizeof(int32_t));
+  al((void**)&p->cand_f, B * cap * sizeof(double));
+  al((void**)&p->coef, B * doa::nj(M) * sizeof(double));
+  if (e != cudaSuccess) {
+    doa_plan_destroy(p);
+    return cuda_fail(e, "doa_plan_create: workspace allocation");
+  }
+  *plan = p;
+  return DOA_OK;
+}
+
+doa_status_t doa_plan_destroy(doa_plan_t p) {
+  if (!p) return DOA_OK;
+  cudaDeviceSynchronize();
+  cudaFree(p->cnt); cudaFree(p->cand_idx); cudaFree(p->cand_f); cudaFree(p->coef);
+  cudaFree(p->R); cudaFree(p->lam); cudaFree(p->V);
+  cudaFree(p->dX[0]); cudaFree(p->dX[1]); cudaFree(p->d_out);
+  if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  for (int k = 0; k < 2; ++k) {
+    if (p->ev_copied[k]) cudaEventDestroy(p->ev_copied[k]);
+    if (p->ev_used[k]) cudaEventDestroy(p->ev_used[k]);
+  }
+  delete p;
+  return DOA_OK;
+}
+
+int32_t doa_plan_capacity(doa_plan_t p) { return p ? p->cap : 0; }
+
+doa_status_t doa_covariance(doa_plan_t p, const float* X, int64_t B, int64_t N, double* R, doa_stream_t s) {
+  g_launches = 0;
+  DOA_CHECK_PLAN(p);
+  DOA_CHECK_B(p, B);
+  if (N < 1) return fail(DOA_ERR_INVALID_ARG, "doa_covariance: N=%lld < 1", (long long)N);
+  if (B == 0) return DOA_OK;
+  DOA_CHECK_PTR(X, 8);
+  DOA_CHECK_PTR(R, 16);
+  DOA_TRY(doa::launch_covariance(X, B, N, p->M, R, (cudaStream_t)s), "doa_covariance");
+  return DOA_OK;
+}
+
+doa_status_t doa_eig(doa_plan_t p, const double* R, int64_t B, double* lambda, double* V, int32_t* info,
+                     doa_stream_t s) {
+  g_launches = 0;
+  DOA_CHECK_PLAN(p);
+  DOA_CHECK_B(p, B);
+  if (B == 0) return DOA_OK;
+  DOA_CHECK_PTR(R, 16);
+  DOA_CHECK_PTR(lambda, 8);
+  DOA_CHECK_PTR(V, 16);
+  DOA_CHECK_PTR(info, 4);
+  DOA_TRY(doa::launch_eig(R, B, p->M, lambda, V, info, (cudaStream_t)s), "doa_eig");
+  return DOA_OK;
+}
+
+doa_status_t doa_spectrum(doa_plan_t p, const double* lambda, const double* V, int64_t B, float* P, int32_t* info,
+                          doa_stream_t s) {
+  g_launches = 0;
+  DOA_CHECK_PLAN(p);
+  DOA_CHECK_B(p, B);
+  if (B == 0) { p->last_B = 0; return DOA_OK; }
+  DOA_CHECK_PTR(lambda, 8);
+  DOA_CHECK_PTR(V, 16);
+  DOA_CHECK_PTR(info, 4);
+  if (P && !aligned(P, 4)) return fail(DOA_ERR_INVALID_ARG, "doa_spectrum: P is not 4-byte aligned");
+  DOA_TRY(doa::launch_coef(p, lambda, V, B, info, (cudaStream_t)s), "doa_spectrum/coef");
+  DOA_TRY(doa::launch_scan(p, B, P, (cudaStream_t)s), "doa_spectrum/scan");
+  p->last_B = B;
+  return DOA_OK;
+}
+
+doa_status_t doa_peaks(doa_plan_t p, int64_t B, int32_t* idx, float* val, int32_t* npk, int32_t* info,
+                       doa_stream_t s) {
+  g_launches = 0;
+  DOA_CHECK_PLAN(p);
+  DOA_CHECK_B(p, B);
+  if (B != p->last_B)
+    return fail(DOA_ERR_INVALID_ARG, "doa_peaks: B=%lld differs from the preceding doa_spectrum (B=%lld)",
+                (long long)B, (long long)p->last_B);
+  if (B == 0) return DOA_OK;
+  DOA_CHECK_PTR(idx, 4);
+  DOA_CHECK_PTR(val, 4);
+  DOA_CHECK_PTR(npk, 4);
+  DOA_CHECK_PTR(info, 4);
+  DOA_TRY(doa::launch_select(p, B, idx, val, npk, info, (cudaStream_t)s), "doa_peaks");
+  return DOA_OK;
+}
+
+doa_status_t doa_run(doa_plan_t p, const float* X, int64_t B, int64_t N, int32_t* idx, float* val, int32_t* npk,
+                     float* P, int32_t* info, doa_stream_t s) {
+  g_launches = 0;
+  DOA_CHECK_PLAN(p);
+  DOA_CHECK_B(p, B);
+  if (N < 1) return fail(DOA_ERR_INVALID_ARG, "doa_run: N=%lld < 1", (long long)N);
+  if (B == 0) return DOA_OK;
+  DOA_CHECK_PTR(X, 8);
+  DOA_CHECK_PTR(idx, 4);
+  DOA_CHECK_PTR(val, 4);
+  DOA_CHECK_PTR(npk, 4);
+  DOA_CHECK_PTR(info, 4);
+  if (P && !aligned(P, 4)) return fail(DOA_ERR_INVALID_ARG, "doa_run: P is not 4-byte aligned");
+  cudaStream_t st = (cudaStream_t)s;
+  DOA_TRY(ensure_run_scratch(p), "doa_run: scratch allocation");
+  DOA_TRY(doa::launch_covariance(X, B, N, p->M, p->R, st), "doa_run/covariance");
+  DOA_TRY(doa::launch_eig(p->R, B, p->M, p->lam, p->V, info, st), "doa_run/eig");
+  DOA_TRY(doa::launch_coef(p, p->lam, p->V, B, info, st), "doa_run/coef");
+  DOA_TRY(doa::launch_scan(p, B, P, st), "doa_run/scan");
+  DOA_TRY(doa::launch_select(p, B, idx, val, npk, info, st), "doa_run/select");
+  p->last_B = B;
+  return DOA_OK;
+}
+
+doa_status_t doa_run_host(const doa_plan_t* plans, int32_t nplans, const float* X_host, int64_t B, int64_t N,
+                          int32_t* idx_host, float* val_host, int32_t* npk_host, int32_t* info_host,
+                          doa_stream_t s) {
+  if (!plans || nplans < 1) return fail(DOA_ERR_INVALID_ARG, "doa_run_host: need nplans >= 1 plans");
+  for (int k = 0; k < nplans; ++k) {
+    if (!plans[k]) return fail(DOA_ERR_INVALID_ARG, "doa_run_host: plans[%d] is NULL", k);
+    if (plans[k]->M != plans[0]->M || plans[k]->D != plans[0]->D)
+      return fail(DOA_ERR_INVALID_ARG, "doa_run_host: plans must share M and D");
+    DOA_CHECK_B(plans[k], B);
+  }
+  doa_plan_s* p = plans[0];
+  if (N < 1) return fail(DOA_ERR_INVALID_ARG, "doa_run_host: N=%lld < 1", (long long)N);
+  if (B == 0) return DOA_OK;
+  if (!X_host || !idx_host || !val_host || !npk_host || !info_host)
+    return fail(DOA_ERR_INVALID_ARG, "doa_run_host: NULL host pointer");
+  cudaStream_t st = (cudaStream_t)s;
+  const int M = p->M, D = p->D;
+  // chunk of frames per H2D copy: ~128 MiB, at most B
+  const size_t frame_bytes = (size_t)N * M * 2 * sizeof(float);
+  int64_t chunk = (int64_t)((128u << 20) / frame_bytes);
+  if (chunk < 1) chunk = 1;
+  if (chunk > B) chunk = B;
+  const size_t need = (size_t)chunk * frame_bytes;
+  DOA_TRY(ensure_run_scratch(p), "doa_run_host: scratch allocation");
+  if (p->dX_bytes < need) {
+    cudaFree(p->dX[0]); cudaFree(p->dX[1]);
+    p->dX[0] = p->dX[1] = nullptr;
+    p->dX_bytes = 0;
+    DOA_TRY(cudaMalloc((void**)&p->dX[0], need), "doa_run_host: staging");
+    DOA_TRY(cudaMalloc((void**)&p->dX[1], need), "doa_run_host: staging");
+    p->dX_bytes = need;
+  }
+  const size_t out_words = (size_t)nplans * p->max_batch * (2 * D + 2);
+  if (p->d_out_words < out_words) {
+    cudaFree(p->d_out);
+    p->d_out = nullptr;
+    p->d_out_words = 0;
+    DOA_TRY(cudaMalloc((void**)&p->d_out, out_words * sizeof(int32_t)), "doa_run_host: outputs");
+    p->d_out_words = out_words;
+  }
+  if (!p->copy_stream) {
+    DOA_TRY(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking), "doa_run_host: stream");
+    for (int k = 0; k < 2; ++k) {
+      DOA_TRY(cudaEventCreateWithFlags(&p->ev_copied[k], cudaEventDisableTiming), "doa_run_host: event");
+      DOA_TRY(cudaEventCreateWithFlags(&p->ev_used[k], cudaEventDisableTiming), "doa_run_host: event");
+    }
+    // buffers start "free"
+    for (int k = 0; k < 2; ++k) DOA_TRY(cudaEventRecord(p->ev_used[k], st), "doa_run_host: record");
+  }
+  int32_t* d_idx = p->d_out;                                              // [nplans][B][D]
+  float* d_val = reinterpret_cast<float*>(d_idx + (size_t)nplans * B * D);  // [nplans][B][D]
+  int32_t* d_npk = reinterpret_cast<int32_t*>(d_val + (size_t)nplans * B * D);  // [nplans][B]
+  int32_t* d_info = d_npk + (size_t)nplans * B;                           // [nplans][B]
+  int launches = 0;
+  int k = 0;
+  for (int64_t b0 = 0; b0 < B; b0 += chunk, k ^= 1) {
+    const int64_t nb = (b0 + chunk <= B) ? chunk : B - b0;
+    // the copy into buffer k may start once the compute that last read it has finished
+    DOA_TRY(cudaStreamWaitEvent(p->copy_stream, p->ev_used[k], 0), "doa_run_host: wait");
+    DOA_TRY(cudaMemcpyAsync(p->dX[k], X_host + (size_t)b0 * N * M * 2, (size_t)nb * frame_bytes,
+                            cudaMemcpyHostToDevice, p->copy_stream), "doa_run_host: H2D");
+    DOA_TRY(cudaEventRecord(p->ev_copied[k], p->copy_stream), "doa_run_host: record");
+    DOA_TRY(cudaStreamWaitEvent(st, p->ev_copied[k], 0), "doa_run_host: wait");
+    g_launches = 0;
+    int32_t* info0 = d_info + b0;                   // plan 0's info slice holds eig flags first
+    DOA_TRY(doa::launch_covariance(p->dX[k], nb, N, M, p->R, st), "doa_run_host/covariance");
+    DOA_TRY(doa::launch_eig(p->R, nb, M, p->lam, p->V, info0, st), "doa_run_host/eig");
+    DOA_TRY(cudaEventRecord(p->ev_used[k], st), "doa_run_host: record");
+    for (int a = 1; a < nplans; ++a)   // every plan starts from the eigensolver's flags
+      DOA_TRY(cudaMemcpyAsync(d_info + (size_t)a * B + b0, info0, (size_t)nb * sizeof(int32_t),
+                              cudaMemcpyDeviceToDevice, st), "doa_run_host: info");
+    for (int a = 0; a < nplans; ++a) {
+      doa_plan_s* q = plans[a];
+      int32_t* inf = d_info + (size_t)a * B + b0;
+      DOA_TRY(doa::launch_coef(q, p->lam, p->V, nb, inf, st), "doa_run_host/coef");
+      DOA_TRY(doa::launch_scan(q, nb, nullptr, st), "doa_run_host/scan");
+      DOA_TRY(doa::launch_select(q, nb, d_idx + ((size_t)a * B + b0) * D, d_val + ((size_t)a * B + b0) * D,
+                                 d_npk + (size_t)a * B + b0, inf, st), "doa_run_host/select");
+      q->last_B = 0;
+    }
+    launches += g_launches;
+  }
+  const size_t nBD = (size_t)nplans * B * D, nB = (size_t)nplans * B;
+  DOA_TRY(cudaMemcpyAsync(idx_host, d_idx, nBD * sizeof(int32_t), cudaMemcpyDeviceToHost, st), "D2H");
+  DOA_TRY(cudaMemcpyAsync(val_host, d_val, nBD * sizeof(float), cudaMemcpyDeviceToHost, st), "D2H");
+  DOA_TRY(cudaMemcpyAsync(npk_host, d_npk, nB * sizeof(int32_t), cudaMemcpyDeviceToHost, st), "D2H");
+  DOA_TRY(cudaMemcpyAsync(info_host, d_info, nB * sizeof(int32_t), cudaMemcpyDeviceToHost, st), "D2H");
+  DOA_TRY(cudaStreamSynchronize(st), "doa_run_host: sync");
+  g_launches = launches;
+  return DOA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,62 @@
+// Internal declarations shared by the libdoa translation units (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../../include/doa.h"
+
+namespace doa {
+
+constexpr int kMaxM = 64;
+constexpr int kMaxSweeps = 30;          // Q15
+constexpr double kFloor = 1e-300;       // Q12
+
+// Coefficient layout per frame (length nj(M) = 2M doubles, "scan-ready"):
+//   coef[0]         = c_0                     (real; trace of C)
+//   coef[k]         = 2 Re c_k,  k = 1..M-1   (multiplies cos(k psi))
+//   coef[M-1+k]     = 2 Im c_k,  k = 1..M-1   (multiplies sin(k psi))
+//   coef[2M-1]      = 0                       (padding)
+// so that f(psi) = sum_j coef[j] T_j(psi) with T = (1, cos psi..cos (M-1)psi, sin psi..sin (M-1)psi, 0)
+// and psi = pi u, u = 2 (d/lambda) sin(theta).  c_k = sum_p C[p][p+k].
+__host__ __device__ constexpr int nj(int M) { return 2 * M; }
+
+}  // namespace doa
+
+struct doa_plan_s {
+  int32_t M, D, alg, cap;
+  double dl, theta0, dtheta;
+  int64_t L, max_batch;
+  int64_t last_B;                 // B of the last doa_spectrum (consumed by doa_peaks)
+  // workspace (device)
+  int32_t* cnt;                   // [max_batch]           candidate counters
+  int32_t* cand_idx;              // [max_batch][cap]
+  double* cand_f;                 // [max_batch][cap]
+  double* coef;                   // [max_batch][2M]
+  double* R;                      // [max_batch][M][M][2]  doa_run scratch
+  double* lam;                    // [max_batch][M]
+  double* V;                      // [max_batch][M][M][2]
+  // doa_run_host staging (lazily sized on first use)
+  float* dX[2];
+  size_t dX_bytes;
+  int32_t* d_out;                 // idx/val/npk/info for nplans x max_batch frames
+  size_t d_out_words;
+  cudaStream_t copy_stream;
+  cudaEvent_t ev_copied[2], ev_used[2];
+};
+
+namespace doa {
+
+// Launchers (enqueue only; return cudaGetLastError() of the launch).  Each increments the
+// thread-local launch counter.
+cudaError_t launch_covariance(const float* X, int64_t B, int64_t N, int M, double* R, cudaStream_t s);
+cudaError_t launch_eig(const double* R, int64_t B, int M, double* lam, double* V, int32_t* info, cudaStream_t s);
+cudaError_t launch_coef(const doa_plan_s* p, const double* lam, const double* V, int64_t B, int32_t* info,
+                        cudaStream_t s);
+cudaError_t launch_scan(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s);
+cudaError_t launch_select(const doa_plan_s* p, int64_t B, int32_t* idx, float* val, int32_t* npk, int32_t* info,
+                          cudaStream_t s);
+
+void count_launch();
+
+}  // namespace doa

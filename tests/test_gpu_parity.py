@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by element on the
+same seeded inputs.  Bars: covariance / eigen-pairs / spectra within stated fp64
+tolerances; peak grid indices exactly equal unless the oracle certifies a tie (Q18); normalised
+pseudo-spectra within 1e-3 dB (north_star, Q17).  Sampled frames at BASELINE.json's full sizes in
+the launch configuration bench.py times.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle as orc  # noqa: E402
+from synth import get_config, generate  # noqa: E402
+from tests.tiecert import certify, delta_bound, max_db_error  # noqa: E402
+
+ALGS = ["phd", "music", "ev", "mn"]
+EPS = np.finfo(float).eps
+
+
+@pytest.fixture(scope="module")
+def doa():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2007_14135_b200 as d
+    return d
+
+
+def _oracle_frame(X, alg, D, dl, theta0, dtheta, L):
+    R = orc.covariance(X)
+    lam, V, sw, info = orc.eig(R)
+    f, _ = orc.spectrum(alg, D, dl, lam, V, theta0, dtheta, L, threads=8)
+    Cm, _ = orc.projector(alg, D, lam, V)
+    idx, fv, npk, n = orc.peaks(f, D)
+    return dict(R=R, lam=lam, V=V, f=f, C=Cm, idx=idx, npk=npk)
+
+
+def _check_frame(o, gidx, gP, alg, M, D, tag, db_tol=1e-3, check_db=True):
+    delta = delta_bound(alg, M, D, o["R"], o["lam"], o["C"], o["f"])
+    ok, ties, why = certify(gidx, o["idx"], o["f"], delta, D)
+    assert ok, f"{tag} {alg}: {why}"
+    if gP is not None and check_db:
+        err = max_db_error(gP, 1.0 / o["f"])
+        assert err <= db_tol, f"{tag} {alg}: dB error {err}"
+    return ties
+
+
+# ------------------------------------------------------------------------------------ per stage
+@pytest.mark.parametrize("M,N,B", [(8, 100, 1), (16, 256, 37), (16, 1024, 3), (7, 50, 5), (64, 300, 2), (2, 1, 3)])
+def test_covariance(doa, M, N, B):
+    rng = np.random.default_rng(M * N + B)
+    X = (rng.standard_normal((B, N, M)) + 1j * rng.standard_normal((B, N, M))).astype(np.complex64)
+    plan = doa.Plan(M, 1, "music", 1.0, max_batch=B)
+    R = plan.covariance(torch.from_numpy(X).cuda()).cpu().numpy()
+    for b in range(B):
+        ref = orc.covariance(X[b])
+        assert np.array_equal(R[b], R[b].conj().T)
+        assert np.all(np.imag(np.diag(R[b])) == 0)
+        assert np.max(np.abs(R[b] - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("M", [2, 3, 7, 8, 16, 17, 32, 64])
+def test_eig_injected_R(doa, M):
+    rng = np.random.default_rng(M)
+    B = 9
+    Rs = []
+    for b in range(B):
+        G = rng.standard_normal((M, 2 * M)) + 1j * rng.standard_normal((M, 2 * M))
+        Rs.append(G @ G.conj().T / (2 * M) * 10.0 ** rng.uniform(-2, 2))
+    Rs = np.stack(Rs)
+    plan = doa.Plan(M, 1, "music", 1.0, max_batch=B)
+    lam, V, info = plan.eig(torch.from_numpy(Rs).cuda())
+    lam, V, info = lam.cpu().numpy(), V.cpu().numpy(), info.cpu().numpy()
+    for b in range(B):
+        R = Rs[b]
+        nR = np.linalg.norm(R)
+        ol, oV, _, _ = orc.eig(R)
+        assert info[b] == 0
+        assert np.all(np.diff(lam[b]) >= 0)
+        assert np.max(np.abs(lam[b] - ol)) <= 1e-13 * nR
+        assert np.linalg.norm(R @ V[b] - V[b] * lam[b]) <= 10 * M * EPS * nR
+        assert np.linalg.norm(V[b].conj().T @ V[b] - np.eye(M)) <= 10 * M * EPS
+        # every eigen-projector of a well-separated eigenvalue matches the oracle's
+        for j in range(M):
+            gap = min([abs(ol[j] - ol[k]) for k in range(M) if k != j])
+            if gap > 1e-6 * nR:
+                Pg = np.outer(V[b][:, j], V[b][:, j].conj())
+                Po = np.outer(oV[:, j], oV[:, j].conj())
+                assert np.linalg.norm(Pg - Po) <= 100 * EPS * nR / gap
+
+
+def test_eig_special_inputs(doa):
+    M = 16
+    Rs = np.stack([np.eye(M, dtype=complex), np.diag(np.arange(M, 0, -1)).astype(complex), np.zeros((M, M), complex)])
+    plan = doa.Plan(M, 1, "music", 1.0, max_batch=3)
+    lam, V, info = plan.eig(torch.from_numpy(Rs).cuda())
+    lam, V = lam.cpu().numpy(), V.cpu().numpy()
+    np.testing.assert_array_equal(lam[0], np.ones(M))
+    np.testing.assert_array_equal(V[0], np.eye(M))
+    np.testing.assert_array_equal(lam[1], np.arange(1, M + 1))
+    np.testing.assert_array_equal(np.abs(V[1]), np.eye(M)[:, ::-1])
+    np.testing.assert_array_equal(lam[2], np.zeros(M))
+
+
+@pytest.mark.parametrize("cfgname", ["c1", "c2", "c3_0.001"])
+@pytest.mark.parametrize("alg", ALGS)
+def test_spectrum_injected_eigs(doa, cfgname, alg):
+    """doa_spectrum + doa_peaks fed the ORACLE's lambda/V: isolates S3-S7."""
+    cfg = get_config(cfgname)
+    X = generate(cfg)[0]
+    o = _oracle_frame(X, alg, cfg.D, cfg.d_over_lambda, cfg.theta0, cfg.dtheta, cfg.L)
+    plan = doa.Plan(cfg.M, cfg.D, alg, cfg.dtheta, L=cfg.L, theta0=cfg.theta0, max_batch=1)
+    lam = torch.from_numpy(o["lam"][None].copy()).cuda()
+    V = torch.from_numpy(o["V"][None].copy()).cuda()
+    P, info = plan.spectrum(lam, V, want_P=True)
+    idx, val, npk, info = plan.peaks(1, info)
+    _check_frame(o, idx.cpu().numpy()[0], P.cpu().numpy()[0], alg, cfg.M, cfg.D, cfgname)
+    # P element-wise: fp32 rounding of 1/f plus fp64 evaluation differences
+    Po = 1.0 / o["f"]
+    Pg = P.cpu().numpy()[0].astype(np.float64)
+    rel = np.abs(Pg - Po) / Po
+    assert np.max(rel) <= 1e-6
+
+
+# ------------------------------------------------------------------------------------ end to end
+@pytest.mark.parametrize("cfgname", ["c1", "c2", "c3_0.1", "c3_0.001"])
+@pytest.mark.parametrize("alg", ALGS)
+def test_run_single_frame(doa, cfgname, alg):
+    cfg = get_config(cfgname)
+    X = generate(cfg)
+    plan = doa.Plan(cfg.M, cfg.D, alg, cfg.dtheta, L=cfg.L, theta0=cfg.theta0, max_batch=1)
+    idx, val, npk, info, P = plan.run(torch.from_numpy(X).cuda(), want_P=True)
+    o = _oracle_frame(X[0], alg, cfg.D, cfg.d_over_lambda, cfg.theta0, cfg.dtheta, cfg.L)
+    _check_frame(o, idx.cpu().numpy()[0], P.cpu().numpy()[0], alg, cfg.M, cfg.D, cfgname)
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_run_c3_finest_grid(doa, alg):
+    """C3 at 0.0001 deg: L = 1,800,001 on one frame (the paper's scan-range sweep)."""
+    cfg = get_config("c3_0.0001")
+    X = generate(cfg)
+    plan = doa.Plan(cfg.M, cfg.D, alg, cfg.dtheta, L=cfg.L, max_batch=1)
+    idx, val, npk, info, P = plan.run(torch.from_numpy(X).cuda(), want_P=True)
+    o = _oracle_frame(X[0], alg, cfg.D, 0.5, -90.0, cfg.dtheta, cfg.L)
+    _check_frame(o, idx.cpu().numpy()[0], P.cpu().numpy()[0], alg, cfg.M, cfg.D, "c3_0.0001")
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_run_batch_ragged(doa, alg):
+    """C4-shaped frames, a batch that spans several scan tiles with ragged tails in B and L."""
+    cfg = get_config("c4").with_(dtheta=0.07)      # L = 2572 (not a multiple of any tile)
+    B = 203
+    X = generate(cfg, frames=range(B))
+    plan = doa.Plan(cfg.M, cfg.D, alg, cfg.dtheta, L=cfg.L, max_batch=B)
+    idx, val, npk, info, P = plan.run(torch.from_numpy(X).cuda(), want_P=True)
+    idx, P, npk, info = idx.cpu().numpy(), P.cpu().numpy(), npk.cpu().numpy(), info.cpu().numpy()
+    r = orc.run_batch(alg, X, cfg.D, 0.5, -90.0, cfg.dtheta, cfg.L, threads=8)
+    for b in range(B):
+        if np.array_equal(idx[b], r["idx"][b]):
+            continue
+        o = _oracle_frame(X[b], alg, cfg.D, 0.5, -90.0, cfg.dtheta, cfg.L)
+        _check_frame(o, idx[b], None, alg, cfg.M, cfg.D, f"frame {b}")
+    for b in range(0, B, 17):
+        o = _oracle_frame(X[b], alg, cfg.D, 0.5, -90.0, cfg.dtheta, cfg.L)
+        assert max_db_error(P[b], 1.0 / o["f"]) <= 1e-3
+    assert np.array_equal(info & ~orc.INFO_UNDERDETERMINED, r["info"] & ~orc.INFO_UNDERDETERMINED)
+
+
+def test_c4_full_size_sampled(doa):
+    """BASELINE configs[3] at full size (65536 frames, L = 18001) in bench.py's launch configuration
+    (covariance + eig once, then spectrum + peaks per algorithm); every 1024th frame + the last
+    checked against the oracle."""
+    cfg = get_config("c4")
+    X = generate(cfg)
+    Xd = torch.from_numpy(X).cuda()
+    sample = list(range(0, cfg.B, 1024)) + [cfg.B - 1]
+    base = doa.Plan(cfg.M, cfg.D, "music", cfg.dtheta, L=cfg.L, max_batch=cfg.B)
+    R = base.covariance(Xd)
+    lam, V, info0 = base.eig(R)
+    orc_frames = {b: orc.eig(orc.covariance(X[b])) for b in sample}
+    for alg in ALGS:
+        plan = doa.Plan(cfg.M, cfg.D, alg, cfg.dtheta, L=cfg.L, max_batch=cfg.B)
+        info = info0.clone()
+        plan.spectrum(lam, V, info)
+        idx, val, npk, info = plan.peaks(cfg.B, info)
+        idx = idx.cpu().numpy()
+        for b in sample:
+            ol, oV, _, _ = orc_frames[b]
+            f, _ = orc.spectrum(alg, cfg.D, 0.5, ol, oV, -90.0, cfg.dtheta, cfg.L, threads=8)
+            oidx = orc.peaks(f, cfg.D)[0]
+            if np.array_equal(idx[b], oidx):
+                continue
+            Cm, _ = orc.projector(alg, cfg.D, ol, oV)
+            o = dict(R=orc.covariance(X[b]), lam=ol, V=oV, f=f, C=Cm, idx=oidx)
+            _check_frame(o, idx[b], None, alg, cfg.M, cfg.D, f"c4 frame {b}")
+        plan.close()
+
+
+# ------------------------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("alg", ALGS)
+def test_edge_zero_input_and_single_snapshot(doa, alg):
+    M, D, L = 8, 2, 181
+    X = np.zeros((2, 4, M), np.complex64)
+    rng = np.random.default_rng(5)
+    X[1, 0] = (rng.standard_normal(M) + 1j * rng.standard_normal(M)).astype(np.complex64)
+    plan = doa.Plan(M, D, alg, 1.0, max_batch=2)
+    idx, val, npk, info, P = plan.run(torch.from_numpy(X).cuda(), want_P=True)
+    idx, P = idx.cpu().numpy(), P.cpu().numpy()
+    assert np.all(np.isfinite(P)) and np.all(P > 0)
+    for b in range(2):
+        o = _oracle_frame(X[b], alg, D, 0.5, -90.0, 1.0, L)
+        _check_frame(o, idx[b], None, alg, M, D, f"edge {b}")
+
+
+@pytest.mark.parametrize("M,D,dl,theta0,dtheta,L", [
+    (2, 1, 0.5, -90.0, 1.0, 181), (5, 2, 0.25, -30.0, 0.05, 1201), (12, 3, 0.8, -60.0, 0.1, 1201),
+    (16, 4, 0.5, -90.0, 60.0, 4), (16, 4, 0.5, 10.0, 0.01, 3), (33, 5, 0.5, -90.0, 0.1, 1801),
+    (64, 8, 0.5, -90.0, 0.05, 3601)])
+def test_geometry_and_grid_variants(doa, M, D, dl, theta0, dtheta, L):
+    cfg = get_config("c2").with_(M=M, D=D, d_over_lambda=dl, N=400,
+                                 sources=tuple(np.linspace(-40, 40, D)), theta0=theta0, dtheta=dtheta)
+    X = generate(cfg, frames=[0, 1])
+    for alg in ALGS:
+        plan = doa.Plan(M, D, alg, dtheta, L=L, theta0=theta0, d_over_lambda=dl, max_batch=2)
+        idx, val, npk, info, P = plan.run(torch.from_numpy(X).cuda(), want_P=True)
+        idx, P = idx.cpu().numpy(), P.cpu().numpy()
+        for b in range(2):
+            o = _oracle_frame(X[b], alg, D, dl, theta0, dtheta, L)
+            _check_frame(o, idx[b], P[b], alg, M, D, f"M={M} dl={dl} b={b}", check_db=L > 3)
+
+
+def test_determinism_and_batch_invariance(doa):
+    cfg = get_config("c4")
+    X = torch.from_numpy(generate(cfg, frames=range(300))).cuda()
+    plan = doa.Plan(cfg.M, cfg.D, "mn", cfg.dtheta, max_batch=300)
+    a = plan.run(X, want_P=True)
+    b = plan.run(X, want_P=True)
+    c = plan.run(X[123:124].contiguous(), want_P=True)
+    for u, v in zip(a, b):
+        assert torch.equal(u, v)
+    assert torch.equal(a[0][123:124], c[0]) and torch.equal(a[4][123:124], c[4])
+
+
+def test_run_host_matches_device(doa):
+    cfg = get_config("c4")
+    Xh = torch.from_numpy(generate(cfg, frames=range(1000))).pin_memory()
+    plan = doa.Plan(cfg.M, cfg.D, "ev", cfg.dtheta, max_batch=1000)
+    d = plan.run(Xh.cuda())
+    h = plan.run_host(Xh)
+    for u, v in zip(d[:4], h):
+        assert torch.equal(u.cpu(), v)
+
+
+def test_invalid_args_enqueue_nothing(doa):
+    plan = doa.Plan(16, 3, "music", 1.0, max_batch=4)
+    X = torch.zeros((5, 10, 16), dtype=torch.complex64, device="cuda")
+    with pytest.raises(doa.DoaError):
+        plan.run(X)                                           # B > max_batch
+    R = torch.zeros((2, 16, 16), dtype=torch.complex128, device="cuda")
+    with pytest.raises(doa.DoaError):
+        doa.doa_covariance(plan.h, X[:2, :0].contiguous(), R)  # N = 0
