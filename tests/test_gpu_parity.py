@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 
 import oracle as orc  # noqa: E402
 from synth import get_config, generate  # noqa: E402
-from tests.tiecert import certify, delta_bound, max_db_error  # noqa: E402
+from tiecert import certify, delta_bound, max_db_error  # noqa: E402
 
 ALGS = ["phd", "music", "ev", "mn"]
 EPS = np.finfo(float).eps
