@@ -122,7 +122,7 @@ doa_status_t doa_plan_create(doa_plan_t* plan, int32_t M, double d_over_lambda, 
   al((void**)&p->cnt, B * sizeof(int32_t));
   al((void**)&p->cand_idx, B * cap * sizeof(int32_t));
   al((void**)&p->cand_f, B * cap * sizeof(double));
-  al((void**)&p->coef, B * doa::nj(M) * sizeof(double));
+  al((void**)&p->coef, doa::coef_words(max_batch, M) * sizeof(double));
   if (e != cudaSuccess) {
     doa_plan_destroy(p);
     return cuda_fail(e, "doa_plan_create: workspace allocation");

@@ -12,14 +12,21 @@ constexpr int kMaxM = 64;
 constexpr int kMaxSweeps = 30;          // Q15
 constexpr double kFloor = 1e-300;       // Q12
 
-// Coefficient layout per frame (length nj(M) = 2M doubles, "scan-ready"):
+// Coefficient vector per frame, K = 4*S entries (S = ksteps(M) k-steps of 4, K >= 2M-1):
 //   coef[0]         = c_0                     (real; trace of C)
 //   coef[k]         = 2 Re c_k,  k = 1..M-1   (multiplies cos(k psi))
 //   coef[M-1+k]     = 2 Im c_k,  k = 1..M-1   (multiplies sin(k psi))
-//   coef[2M-1]      = 0                       (padding)
-// so that f(psi) = sum_j coef[j] T_j(psi) with T = (1, cos psi..cos (M-1)psi, sin psi..sin (M-1)psi, 0)
+//   coef[j]         = 0,         j >= 2M-1    (padding)
+// so that f(psi) = sum_j coef[j] T_j(psi) with T = (1, cos psi..cos (M-1)psi, sin psi..sin (M-1)psi, 0..)
 // and psi = pi u, u = 2 (d/lambda) sin(theta).  c_k = sum_p C[p][p+k].
-__host__ __device__ constexpr int nj(int M) { return 2 * M; }
+// Stored in the DMMA A-fragment order of 8-frame groups: element (b, j) lives at
+//   ((b/8)*S + j/4)*32 + (b%8)*4 + j%4
+// so one coalesced 8-byte load per k-step gives every lane its m8n8k4 A operand.
+__host__ __device__ constexpr int ksteps(int M) { return (2 * M + 3) / 4; }
+__host__ __device__ inline size_t coef_index(int64_t b, int j, int S) {
+  return ((size_t)(b >> 3) * S + (j >> 2)) * 32 + (size_t)(b & 7) * 4 + (j & 3);
+}
+inline size_t coef_words(int64_t max_batch, int M) { return (size_t)((max_batch + 7) / 8) * ksteps(M) * 32; }
 
 }  // namespace doa
 

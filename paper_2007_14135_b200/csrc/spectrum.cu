@@ -6,7 +6,8 @@
 //     a^H C a = sum_{p,q} C_pq z^{q-p} = c_0 + 2 Re sum_{k>=1} c_k z^k,   c_k = sum_p C[p][p+k].
 // Each (frame, angle) then costs 2(M-1) fp64 FMAs against a per-angle table
 // T(psi) = (1, cos k psi, sin k psi) shared by every frame — the scan is the real contraction
-// F[b][i] = sum_j coef[b][j] T[j][i] with K = 2M (Table 2 Step-5).
+// F[b][i] = sum_j coef[b][j] T[j][i] (Table 2 Step-5), K = 4S >= 2M-1, run on the FP64
+// tensor pipe (DMMA, mma.sync m8n8k4 f64) with the table resident in registers.
 #include <cfloat>
 
 #include "doa_internal.cuh"
@@ -25,7 +26,8 @@ __device__ __forceinline__ float to_p32(double f) {
 //   PHD: u = e_0 (smallest eigenvalue), w = 1.     MUSIC: u_j = e_j, j < K = M-D, w = 1.
 //   EV : u_j = e_j, w_j = 1/lambda_j (Q1), clamped at 100 eps lambda_max (DEGENERATE).
 //   MN : u = P_n e1 / (e1^H P_n e1), P_n e1 = sum_j e_j conj(e_j[0]) (Q5); p0 <= 100 eps: DEGENERATE.
-// Also zeroes the frame's candidate counter for the scan that follows.
+// Writes the coefficients in the scan's A-fragment layout (coef_index) and zeroes the frame's
+// candidate counter for the scan that follows.
 __global__ void __launch_bounds__(128) coef_kernel(const double* __restrict__ lam, const double2* __restrict__ V,
                                                   int64_t B, int M, int D, int alg, double* __restrict__ coef,
                                                   int32_t* __restrict__ cnt, int32_t* __restrict__ info) {
@@ -33,6 +35,7 @@ __global__ void __launch_bounds__(128) coef_kernel(const double* __restrict__ la
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t b = (int64_t)blockIdx.x * 4 + warp;
   if (b >= B) return;
+  const int S = ksteps(M);
   const double2* Vb = V + (size_t)b * M * M;
   const double* lb = lam + (size_t)b * M;
   const int K = M - D;
@@ -62,7 +65,6 @@ __global__ void __launch_bounds__(128) coef_kernel(const double* __restrict__ la
     }
     __syncwarp();
   }
-  double* cb = coef + (size_t)b * nj(M);
   for (int k = lane; k < M; k += 32) {
     double cr = 0.0, ci = 0.0;
     for (int j = 0; j < nv; ++j) {
@@ -80,111 +82,169 @@ __global__ void __launch_bounds__(128) coef_kernel(const double* __restrict__ la
       cr += w * sr;
       ci += w * si;
     }
-    if (k == 0) { cb[0] = cr; cb[2 * M - 1] = 0.0; }
-    else { cb[k] = 2.0 * cr; cb[M - 1 + k] = 2.0 * ci; }
+    if (k == 0) coef[coef_index(b, 0, S)] = cr;
+    else {
+      coef[coef_index(b, k, S)] = 2.0 * cr;
+      coef[coef_index(b, M - 1 + k, S)] = 2.0 * ci;
+    }
   }
+  for (int j = 2 * M - 1 + lane; j < 4 * S; j += 32) coef[coef_index(b, j, S)] = 0.0;   // K padding
   if (lane == 0) {
     cnt[b] = 0;
     if (info) info[b] |= flag;
   }
 }
 
+// T_j(psi): j = 0 -> 1; 1..M-1 -> cos(j psi); M..2M-2 -> sin((j-M+1) psi); else 0.
+// psi = pi u; cospi/sinpi of the exact multiple j*u (one rounding) — no recurrence.
+__device__ __forceinline__ double table_entry(int j, int M, double u) {
+  if (j == 0) return 1.0;
+  if (j < M) return cospi((double)j * u);
+  if (j < 2 * M - 1) return sinpi((double)(j - M + 1) * u);
+  return 0.0;
+}
+
+__device__ __forceinline__ double grid_u(int64_t i, double theta0, double dtheta, double dl) {
+  const double th = __dadd_rn(__dmul_rn((double)i, dtheta), theta0);   // Q8: multiply then add
+  return 2.0 * dl * sinpi(th / 180.0);                                    // u = 2 (d/lambda) sin(theta)
+}
+
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 // ---------------------------------------------------------------------------------------------
-// S4-S6 (first version, DFMA): each lane owns one angle of a 32-angle warp block whose end lanes
-// are halo (lanes 1..30 decide; warp stride 30).  The lane's table T (2M doubles) is generated
-// once in registers with fp64 sincospi, then the CTA's frame range is streamed: per frame a
-// warp-uniform coefficient load, 2M-1 DFMAs, a neighbour exchange by shuffles and the peak test
-// f_i < f_{i-1} && f_i <= f_{i+1} on interior indices (Q9/Q10).
+// S4-S6 on the FP64 tensor pipe.  A warp owns a block of W = 8*NA consecutive grid angles
+// (positions 0 and W-1 are halo; warp blocks advance by W-2 so every interior angle is decided
+// by exactly one lane) and a range of frame groups (8 frames each).
+//   B-fragments (the steering table): lane holds T_{4s + lane%4}(angle 8t + lane/4), s < S,
+//     t < NA — generated once per warp with fp64 sincospi and kept in registers.
+//   A-fragments (coefficients): coef[8g + lane/4][4s + lane%4], one coalesced 8-byte load per s.
+//   D (8 frames x 8 angles per t): lane holds frame lane/4, angles 8t + 2(lane%4) + {0,1}.
+// Epilogue per group: floor (Q12), neighbour values by shuffles inside each 4-lane frame row,
+// peak test f_i < f_{i-1} && f_i <= f_{i+1} on interior indices (Q9/Q10), rare atomic append to
+// the frame's candidate list, optional fp32 P store.
 constexpr int kScanWarps = 4;
-constexpr int kScanStride = 30;
 
 template <int M>
-__global__ void __launch_bounds__(kScanWarps * 32) scan_kernel(const double* __restrict__ coef, int64_t B,
-                                                              int64_t frames_per_cta, double dl, double theta0,
-                                                              double dtheta, int64_t L, int cap,
-                                                              int32_t* __restrict__ cnt, int32_t* __restrict__ cidx,
-                                                              double* __restrict__ cf, float* __restrict__ P) {
-  constexpr int NJ = nj(M);
+struct ScanShape {
+  static constexpr int S = (2 * M + 3) / 4;                 // k-steps of 4
+  static constexpr int NA = (64 / S) < 8 ? (64 / S) : 8;    // 8-angle tiles per warp
+  static constexpr int W = 8 * NA;                           // angles per warp block (incl. 2 halo)
+};
+
+template <int M>
+__global__ void __launch_bounds__(kScanWarps * 32) scan_dmma_kernel(const double* __restrict__ coef, int64_t B,
+                                                                   int64_t groups_per_cta, double dl,
+                                                                   double theta0, double dtheta, int64_t L,
+                                                                   int cap, int32_t* __restrict__ cnt,
+                                                                   int32_t* __restrict__ cidx,
+                                                                   double* __restrict__ cf,
+                                                                   float* __restrict__ P) {
+  constexpr int S = ScanShape<M>::S, NA = ScanShape<M>::NA, W = ScanShape<M>::W;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane & 3, r = lane >> 2;
   const int64_t wblk = (int64_t)blockIdx.x * kScanWarps + warp;
-  const int64_t i = wblk * kScanStride - 1 + lane;
-  const bool valid = (i >= 0 && i < L);
-  double T[NJ];
-  T[0] = 1.0;
-  if (valid) {
-    const double th = __dadd_rn(__dmul_rn((double)i, dtheta), theta0);   // Q8: multiply then add
-    const double u = 2.0 * dl * sinpi(th / 180.0);
+  const int64_t base = wblk * (W - 2) - 1;                     // grid index of position 0
+  if (base + 1 >= L) return;                                   // whole warp beyond the grid
+
+  double tf[NA][S];
 #pragma unroll
-    for (int k = 1; k < M; ++k) {
-      double s, c;
-      sincospi((double)k * u, &s, &c);
-      T[k] = c;
-      T[M - 1 + k] = s;
-    }
-  } else {
+  for (int t = 0; t < NA; ++t) {
+    const int64_t i = base + 8 * t + r;
+    const bool valid = (i >= 0 && i < L);
+    const double u = valid ? grid_u(i, theta0, dtheta, dl) : 0.0;
 #pragma unroll
-    for (int k = 1; k < M; ++k) { T[k] = 0.0; T[M - 1 + k] = 0.0; }
+    for (int s = 0; s < S; ++s) tf[t][s] = valid ? table_entry(4 * s + q, M, u) : (4 * s + q == 0 ? 1.0 : 0.0);
   }
-  const bool own = lane >= 1 && lane <= kScanStride && valid;
-  const bool decide = own && i >= 1 && i <= L - 2;
-  const int64_t b0 = (int64_t)blockIdx.y * frames_per_cta;
-  const int64_t b1 = min(B, b0 + frames_per_cta);
-  for (int64_t b = b0; b < b1; ++b) {
-    const double* cb = coef + (size_t)b * NJ;
-    double acc = __ldg(cb);
+
+  const int64_t ngroups = (B + 7) / 8;
+  const int64_t g0 = (int64_t)blockIdx.y * groups_per_cta;
+  const int64_t g1 = (g0 + groups_per_cta < ngroups) ? g0 + groups_per_cta : ngroups;
+  for (int64_t g = g0; g < g1; ++g) {
+    double a[S];
 #pragma unroll
-    for (int j = 1; j < NJ - 1; ++j) acc = fma(__ldg(cb + j), T[j], acc);
-    const double f = acc > kFloor ? acc : kFloor;
-    const double fl = __shfl_up_sync(0xffffffffu, f, 1);
-    const double fr = __shfl_down_sync(0xffffffffu, f, 1);
-    if (decide && f < fl && f <= fr) {
-      const int slot = atomicAdd(cnt + b, 1);
-      if (slot < cap) {
-        cidx[(size_t)b * cap + slot] = (int32_t)i;
-        cf[(size_t)b * cap + slot] = f;
+    for (int s = 0; s < S; ++s) a[s] = __ldg(coef + ((size_t)g * S + s) * 32 + lane);
+    double acc[NA][2];
+#pragma unroll
+    for (int t = 0; t < NA; ++t) { acc[t][0] = 0.0; acc[t][1] = 0.0; }
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+      for (int t = 0; t < NA; ++t) dmma_884(acc[t][0], acc[t][1], a[s], tf[t][s]);
+
+    const int64_t b = g * 8 + r;
+    const bool frame_ok = b < B;
+#pragma unroll
+    for (int t = 0; t < NA; ++t) {
+      acc[t][0] = acc[t][0] > kFloor ? acc[t][0] : kFloor;
+      acc[t][1] = acc[t][1] > kFloor ? acc[t][1] : kFloor;
+    }
+    // neighbours: left of (t,q,0) is (t,q-1,1) [q>0] or (t-1,3,1) [q=0];
+    //             right of (t,q,1) is (t,q+1,0) [q<3] or (t+1,0,0) [q=3]
+    const int srcL = q > 0 ? lane - 1 : lane + 3;
+    const int srcR = q < 3 ? lane + 1 : lane - 3;
+    double up[NA], dn[NA];
+#pragma unroll
+    for (int t = 0; t < NA; ++t) {
+      up[t] = __shfl_sync(0xffffffffu, acc[t][1], srcL);
+      dn[t] = __shfl_sync(0xffffffffu, acc[t][0], srcR);
+    }
+#pragma unroll
+    for (int t = 0; t < NA; ++t) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int pos = 8 * t + 2 * q + e;
+        const int64_t i = base + pos;
+        const double f = acc[t][e];
+        double fl, fr;
+        if (e == 0) { fl = q > 0 ? up[t] : (t > 0 ? up[t - 1] : f); fr = acc[t][1]; }
+        else { fl = acc[t][0]; fr = q < 3 ? dn[t] : (t + 1 < NA ? dn[t + 1] : f); }
+        const bool inner = pos >= 1 && pos <= W - 2;
+        if (frame_ok && inner && i >= 1 && i <= L - 2 && f < fl && f <= fr) {
+          const int slot = atomicAdd(cnt + b, 1);
+          if (slot < cap) {
+            cidx[(size_t)b * cap + slot] = (int32_t)i;
+            cf[(size_t)b * cap + slot] = f;
+          }
+        }
+        if (P && frame_ok && inner && i < L) P[(size_t)b * L + i] = to_p32(f);
       }
     }
-    if (P && own) P[(size_t)b * L + i] = to_p32(f);
   }
 }
 
-// Same algorithm for any M <= 64 with the table in shared memory (runtime M; used for M > 32,
-// where a register-resident table would spill).
-__global__ void __launch_bounds__(kScanWarps * 32) scan_kernel_smem(const double* __restrict__ coef, int64_t B, int M,
+// Same contraction for any M <= 64 with the table in shared memory and plain DFMA (runtime M;
+// used for M > 32, where a register-resident table would spill).  Lanes own angles of a
+// 32-angle block with halo lanes 0 and 31 (stride 30).
+constexpr int kSmemStride = 30;
+
+__global__ void __launch_bounds__(kScanWarps * 32) scan_smem_kernel(const double* __restrict__ coef, int64_t B, int M,
                                                                    int64_t frames_per_cta, double dl, double theta0,
                                                                    double dtheta, int64_t L, int cap,
                                                                    int32_t* __restrict__ cnt,
                                                                    int32_t* __restrict__ cidx, double* __restrict__ cf,
                                                                    float* __restrict__ P) {
   extern __shared__ double tsm[];
-  const int NJ = nj(M);
+  const int S = ksteps(M);
+  const int NJ = 4 * S;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* T = tsm + (size_t)warp * NJ * 32;          // T[j][lane]
   const int64_t wblk = (int64_t)blockIdx.x * kScanWarps + warp;
-  const int64_t i = wblk * kScanStride - 1 + lane;
+  const int64_t i = wblk * kSmemStride - 1 + lane;
   const bool valid = (i >= 0 && i < L);
-  T[lane] = 1.0;
-  T[(NJ - 1) * 32 + lane] = 0.0;
-  double u = 0.0;
-  if (valid) {
-    const double th = __dadd_rn(__dmul_rn((double)i, dtheta), theta0);
-    u = 2.0 * dl * sinpi(th / 180.0);
-  }
-  for (int k = 1; k < M; ++k) {
-    double sn = 0.0, c = 0.0;
-    if (valid) sincospi((double)k * u, &sn, &c);
-    T[k * 32 + lane] = c;
-    T[(M - 1 + k) * 32 + lane] = sn;
-  }
+  const double u = valid ? grid_u(i, theta0, dtheta, dl) : 0.0;
+  for (int j = 0; j < NJ; ++j) T[j * 32 + lane] = valid ? table_entry(j, M, u) : (j == 0 ? 1.0 : 0.0);
   __syncwarp();
-  const bool own = lane >= 1 && lane <= kScanStride && valid;
+  const bool own = lane >= 1 && lane <= kSmemStride && valid;
   const bool decide = own && i >= 1 && i <= L - 2;
   const int64_t b0 = (int64_t)blockIdx.y * frames_per_cta;
-  const int64_t b1 = min(B, b0 + frames_per_cta);
+  const int64_t b1 = (b0 + frames_per_cta < B) ? b0 + frames_per_cta : B;
   for (int64_t b = b0; b < b1; ++b) {
-    const double* cb = coef + (size_t)b * NJ;
-    double acc = __ldg(cb);
-    for (int j = 1; j < NJ - 1; ++j) acc = fma(__ldg(cb + j), T[j * 32 + lane], acc);
+    double acc = __ldg(coef + coef_index(b, 0, S));
+    for (int j = 1; j < 2 * M - 1; ++j) acc = fma(__ldg(coef + coef_index(b, j, S)), T[j * 32 + lane], acc);
     const double f = acc > kFloor ? acc : kFloor;
     const double fl = __shfl_up_sync(0xffffffffu, f, 1);
     const double fr = __shfl_down_sync(0xffffffffu, f, 1);
@@ -199,23 +259,25 @@ __global__ void __launch_bounds__(kScanWarps * 32) scan_kernel_smem(const double
   }
 }
 
-int64_t scan_frames_per_cta(int64_t gx, int64_t B) {
-  // frame chunk: enough CTAs for ~8 waves on 148 SMs, at least 16 frames per CTA
-  int64_t fpc = (gx * B) / (148 * 16 * 8);
-  fpc = fpc < 16 ? 16 : fpc;
-  if (fpc > B) fpc = B;
-  return fpc;
+int64_t waves_chunk(int64_t cols, int64_t units, int64_t min_per_cta) {
+  // split `units` (frame groups or frames) into chunks so the grid has ~8 waves of 148 SMs x 2 CTAs
+  int64_t per = (cols * units) / (148 * 2 * 8);
+  if (per < min_per_cta) per = min_per_cta;
+  if (per > units) per = units;
+  return per;
 }
 
 template <int M>
 cudaError_t launch_scan_t(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
-  const int64_t nwb = (p->L + kScanStride - 1) / kScanStride;
+  constexpr int W = ScanShape<M>::W;
+  const int64_t nwb = (p->L + (W - 2) - 1) / (W - 2);           // warp blocks owning [0, L)
   const int64_t gx = (nwb + kScanWarps - 1) / kScanWarps;
-  const int64_t fpc = scan_frames_per_cta(gx, B);
-  const int64_t gy = (B + fpc - 1) / fpc;
+  const int64_t ngroups = (B + 7) / 8;
+  const int64_t per = waves_chunk(gx, ngroups, 8);
+  const int64_t gy = (ngroups + per - 1) / per;
   count_launch();
-  scan_kernel<M><<<dim3((unsigned)gx, (unsigned)gy), kScanWarps * 32, 0, s>>>(
-      p->coef, B, fpc, p->dl, p->theta0, p->dtheta, p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
+  scan_dmma_kernel<M><<<dim3((unsigned)gx, (unsigned)gy), kScanWarps * 32, 0, s>>>(
+      p->coef, B, per, p->dl, p->theta0, p->dtheta, p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
   return cudaGetLastError();
 }
 
@@ -280,19 +342,19 @@ cudaError_t launch_scan(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s
     DOA_SCAN_CASE(30) DOA_SCAN_CASE(31) DOA_SCAN_CASE(32)
 #undef DOA_SCAN_CASE
     default: {
-      const int64_t nwb = (p->L + kScanStride - 1) / kScanStride;
+      const int64_t nwb = (p->L + kSmemStride - 1) / kSmemStride;
       const int64_t gx = (nwb + kScanWarps - 1) / kScanWarps;
-      const int64_t fpc = scan_frames_per_cta(gx, B);
+      const int64_t fpc = waves_chunk(gx, B, 16);
       const int64_t gy = (B + fpc - 1) / fpc;
-      const size_t smem = (size_t)kScanWarps * nj(p->M) * 32 * sizeof(double);
+      const size_t smem = (size_t)kScanWarps * 4 * ksteps(p->M) * 32 * sizeof(double);
       static bool attr = false;
       if (!attr) {
-        cudaFuncSetAttribute(scan_kernel_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kScanWarps * nj(kMaxM) * 32 * sizeof(double)));
+        cudaFuncSetAttribute(scan_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kScanWarps * 4 * ksteps(kMaxM) * 32 * sizeof(double)));
         attr = true;
       }
       count_launch();
-      scan_kernel_smem<<<dim3((unsigned)gx, (unsigned)gy), kScanWarps * 32, smem, s>>>(
+      scan_smem_kernel<<<dim3((unsigned)gx, (unsigned)gy), kScanWarps * 32, smem, s>>>(
           p->coef, B, p->M, fpc, p->dl, p->theta0, p->dtheta, p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
       return cudaGetLastError();
     }
