@@ -11,7 +11,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdoa.so")
+LIB_PATH = os.environ.get("DOA_LIB") or os.path.join(_HERE, "libdoa.so")   # DOA_LIB: tuning builds only
 
 ALG = {"phd": 0, "music": 1, "ev": 2, "mn": 3}
 INFO_NOCONV, INFO_DEGENERATE, INFO_CAND_OVERFLOW, INFO_UNDERDETERMINED = 1, 2, 4, 8

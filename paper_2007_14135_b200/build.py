@@ -30,11 +30,11 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in sources() + headers())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    if out == LIB and not force and not stale():
         return LIB
-    tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", tmp, *sources()]
+    tmp = out + ".tmp"
+    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-o", tmp, *sources()]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
@@ -43,9 +43,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         fh.write(r.stderr)
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose=True, out=outs[0] if outs else LIB, defines=defs))

@@ -1,0 +1,107 @@
+// S1 for M <= 16 on the FP64 tensor pipe: R = (1/N) X X^H (Eq. 3; Table 2 Step-1).
+//
+// With Y = [Re X^T; Im X^T] (2*16 x N, rows padded to 16 per half), the real Gram matrix
+// G = Y Y^T gives R = (G_rr + G_ii) + j (G_ir - G_ri) blockwise.  One warp per frame computes the
+// ten 8x8 tiles of the upper block triangle of G with mma.sync m8n8k4 f64: for k-step n0 every
+// lane loads the two complex64 samples x_{n0+q}[r] and x_{n0+q}[8+r] (r = lane/4, q = lane%4),
+// converts them once, and the same four doubles serve as both the A fragment (row block I) and the
+// B fragment (column block J) of every tile (I, J).  fp32 products are exact in fp64; sums are
+// fp64 in the DMMA's fixed order (deterministic).  The tiles are then mirrored through shared
+// memory and combined into the full Hermitian R (exact conjugate mirror, real diagonal).
+#include "doa_internal.cuh"
+
+namespace doa {
+namespace {
+
+constexpr int kCovWarps = 4;
+constexpr int kGld = 33;          // smem row stride of the 32x32 Gram matrix (doubles)
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// tile list (I <= J) over the 4 row blocks {Re 0-7, Re 8-15, Im 0-7, Im 8-15}
+__device__ constexpr int kTI[10] = {0, 0, 1, 2, 2, 3, 0, 0, 1, 1};
+__device__ constexpr int kTJ[10] = {0, 1, 1, 2, 3, 3, 2, 3, 2, 3};
+
+__global__ void __launch_bounds__(kCovWarps * 32) cov16_kernel(const float2* __restrict__ X, int64_t B, int64_t N,
+                                                             int M, double2* __restrict__ R) {
+  __shared__ double Gs[kCovWarps][32 * kGld];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t b = (int64_t)blockIdx.x * kCovWarps + warp;
+  if (b >= B) return;
+  const int r = lane >> 2, q = lane & 3;
+  const float2* Xb = X + (size_t)b * N * M;
+  const bool lo_ok = r < M, hi_ok = r + 8 < M;
+
+  double acc[10][2];
+#pragma unroll
+  for (int t = 0; t < 10; ++t) { acc[t][0] = 0.0; acc[t][1] = 0.0; }
+
+  constexpr int U = 8;                       // k-steps in flight per warp
+  int64_t n0 = 0;
+  for (; n0 + 4 * U <= N; n0 += 4 * U) {
+    float2 x0[U], x1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float2* row = Xb + (size_t)(n0 + 4 * u + q) * M;
+      x0[u] = lo_ok ? __ldg(row + r) : make_float2(0.f, 0.f);
+      x1[u] = hi_ok ? __ldg(row + r + 8) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double y[4] = {(double)x0[u].x, (double)x1[u].x, (double)x0[u].y, (double)x1[u].y};
+#pragma unroll
+      for (int t = 0; t < 10; ++t) dmma(acc[t][0], acc[t][1], y[kTI[t]], y[kTJ[t]]);
+    }
+  }
+  for (; n0 < N; n0 += 4) {                  // ragged tail (N not a multiple of 32)
+    const int64_t n = n0 + q;
+    float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+    if (n < N) {
+      const float2* row = Xb + (size_t)n * M;
+      if (lo_ok) a0 = __ldg(row + r);
+      if (hi_ok) a1 = __ldg(row + r + 8);
+    }
+    const double y[4] = {(double)a0.x, (double)a1.x, (double)a0.y, (double)a1.y};
+#pragma unroll
+    for (int t = 0; t < 10; ++t) dmma(acc[t][0], acc[t][1], y[kTI[t]], y[kTJ[t]]);
+  }
+
+  // D fragment of tile (I, J): lane holds G[8I + r][8J + 2q + e]; store G and its mirror
+  double* G = Gs[warp];
+#pragma unroll
+  for (int t = 0; t < 10; ++t) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int i = 8 * kTI[t] + r, j = 8 * kTJ[t] + 2 * q + e;
+      G[i * kGld + j] = acc[t][e];
+      G[j * kGld + i] = acc[t][e];
+    }
+  }
+  __syncwarp();
+  const double dn = (double)N;
+  double2* Rb = R + (size_t)b * M * M;
+  for (int e = lane; e < M * M; e += 32) {
+    const int i = e / M, j = e - (e / M) * M;
+    if (i > j) continue;
+    const double re = G[i * kGld + j] + G[(16 + i) * kGld + 16 + j];
+    const double im = G[(16 + i) * kGld + j] - G[i * kGld + 16 + j];
+    const double2 v = make_double2(re / dn, i == j ? 0.0 : im / dn);
+    Rb[(size_t)i * M + j] = v;
+    if (i != j) Rb[(size_t)j * M + i] = make_double2(v.x, -v.y);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_cov16(const float* X, int64_t B, int64_t N, int M, double* R, cudaStream_t s) {
+  count_launch();
+  cov16_kernel<<<(unsigned)((B + kCovWarps - 1) / kCovWarps), kCovWarps * 32, 0, s>>>(
+      reinterpret_cast<const float2*>(X), B, N, M, reinterpret_cast<double2*>(R));
+  return cudaGetLastError();
+}
+
+}  // namespace doa

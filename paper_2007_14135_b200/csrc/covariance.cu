@@ -109,7 +109,10 @@ __global__ void __launch_bounds__(kCovThreads) covariance_kernel(const float2* _
 
 }  // namespace
 
+cudaError_t launch_cov16(const float* X, int64_t B, int64_t N, int M, double* R, cudaStream_t s);
+
 cudaError_t launch_covariance(const float* X, int64_t B, int64_t N, int M, double* R, cudaStream_t s) {
+  if (M <= 16) return launch_cov16(X, B, N, M, R, s);
   const int Mp = (M + 1) & ~1;
   const int nb = Mp / 2, nblk = nb * (nb + 1) / 2;
   const int nslice = nblk >= kCovThreads ? 1 : kCovThreads / nblk;

@@ -12,6 +12,7 @@
 // off(A) = sqrt(sum_{i!=j} |a_ij|^2) <= 10 eps ||R||_F evaluated directly at the start of every
 // sweep, capped at 30 sweeps (Q15).  Eigenvalues are sorted ascending, ties by index (Q2).
 #include <cfloat>
+#include <cstdlib>
 
 #include "doa_internal.cuh"
 
@@ -174,7 +175,11 @@ cudaError_t launch_eig_t(const double* R, int64_t B, int M, double* lam, double*
 
 }  // namespace
 
+cudaError_t launch_eig16(const double* R, int64_t B, int M, double* lam, double* V, int32_t* info, cudaStream_t s);
+
 cudaError_t launch_eig(const double* R, int64_t B, int M, double* lam, double* V, int32_t* info, cudaStream_t s) {
+  static const bool legacy = getenv("DOA_EIG_SMEM") != nullptr;   // A/B switch for tuning only
+  if (M <= 16 && !legacy) return launch_eig16(R, B, M, lam, V, info, s);
   if (M <= 16) return launch_eig_t<16, 4>(R, B, M, lam, V, info, s);
   if (M <= 32) return launch_eig_t<32, 2>(R, B, M, lam, V, info, s);
   return launch_eig_t<64, 1>(R, B, M, lam, V, info, s);

@@ -127,46 +127,65 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 // peak test f_i < f_{i-1} && f_i <= f_{i+1} on interior indices (Q9/Q10), rare atomic append to
 // the frame's candidate list, optional fp32 P store.
 constexpr int kScanWarps = 4;
+#ifndef DOA_SCAN_MINB
+#define DOA_SCAN_MINB 2
+#endif
 
-template <int M>
+template <int M, int NA_ = 0>
 struct ScanShape {
   static constexpr int S = (2 * M + 3) / 4;                 // k-steps of 4
-  static constexpr int NA = (64 / S) < 8 ? (64 / S) : 8;    // 8-angle tiles per warp
+  static constexpr int NA_default = (64 / S) < 8 ? (64 / S) : 8;
+  static constexpr int NA = NA_ > 0 ? NA_ : NA_default;     // 8-angle tiles per warp
   static constexpr int W = 8 * NA;                           // angles per warp block (incl. 2 halo)
 };
 
-template <int M>
-__global__ void __launch_bounds__(kScanWarps * 32) scan_dmma_kernel(const double* __restrict__ coef, int64_t B,
+template <int M, int NA, bool WRITE_P>
+__global__ void __launch_bounds__(kScanWarps * 32, DOA_SCAN_MINB) scan_dmma_kernel(const double* __restrict__ coef, int64_t B,
                                                                    int64_t groups_per_cta, double dl,
-                                                                   double theta0, double dtheta, int64_t L,
+                                                                   double theta0, double dtheta, int L,
                                                                    int cap, int32_t* __restrict__ cnt,
                                                                    int32_t* __restrict__ cidx,
                                                                    double* __restrict__ cf,
                                                                    float* __restrict__ P) {
-  constexpr int S = ScanShape<M>::S, NA = ScanShape<M>::NA, W = ScanShape<M>::W;
+  constexpr int S = ScanShape<M, NA>::S, W = ScanShape<M, NA>::W;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q = lane & 3, r = lane >> 2;
-  const int64_t wblk = (int64_t)blockIdx.x * kScanWarps + warp;
-  const int64_t base = wblk * (W - 2) - 1;                     // grid index of position 0
+  const int wblk = blockIdx.x * kScanWarps + warp;
+  const int base = wblk * (W - 2) - 1;                         // grid index of position 0 (L < 2^31)
   if (base + 1 >= L) return;                                   // whole warp beyond the grid
 
   double tf[NA][S];
 #pragma unroll
   for (int t = 0; t < NA; ++t) {
-    const int64_t i = base + 8 * t + r;
+    const int i = base + 8 * t + r;
     const bool valid = (i >= 0 && i < L);
     const double u = valid ? grid_u(i, theta0, dtheta, dl) : 0.0;
 #pragma unroll
     for (int s = 0; s < S; ++s) tf[t][s] = valid ? table_entry(4 * s + q, M, u) : (4 * s + q == 0 ? 1.0 : 0.0);
   }
+  // this lane's D positions (t, e) -> grid index base + 8t + 2q + e.  decide: interior of the
+  // warp block and of the grid (Q9); own: interior of the warp block and inside the grid.
+  unsigned dmask = 0, omask = 0;
+#pragma unroll
+  for (int t = 0; t < NA; ++t)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int pos = 8 * t + 2 * q + e, i = base + pos;
+      const bool inner = pos >= 1 && pos <= W - 2;
+      if (inner && i >= 1 && i <= L - 2) dmask |= 1u << (2 * t + e);
+      if (inner && i >= 0 && i < L) omask |= 1u << (2 * t + e);
+    }
+  const int srcL = q > 0 ? lane - 1 : lane + 3;
+  const int srcR = q < 3 ? lane + 1 : lane - 3;
 
   const int64_t ngroups = (B + 7) / 8;
   const int64_t g0 = (int64_t)blockIdx.y * groups_per_cta;
   const int64_t g1 = (g0 + groups_per_cta < ngroups) ? g0 + groups_per_cta : ngroups;
-  for (int64_t g = g0; g < g1; ++g) {
+  const double* cg = coef + ((size_t)g0 * S) * 32 + lane;
+  for (int64_t g = g0; g < g1; ++g, cg += S * 32) {
     double a[S];
 #pragma unroll
-    for (int s = 0; s < S; ++s) a[s] = __ldg(coef + ((size_t)g * S + s) * 32 + lane);
+    for (int s = 0; s < S; ++s) a[s] = __ldg(cg + s * 32);
     double acc[NA][2];
 #pragma unroll
     for (int t = 0; t < NA; ++t) { acc[t][0] = 0.0; acc[t][1] = 0.0; }
@@ -175,42 +194,52 @@ __global__ void __launch_bounds__(kScanWarps * 32) scan_dmma_kernel(const double
 #pragma unroll
       for (int t = 0; t < NA; ++t) dmma_884(acc[t][0], acc[t][1], a[s], tf[t][s]);
 
-    const int64_t b = g * 8 + r;
-    const bool frame_ok = b < B;
 #pragma unroll
-    for (int t = 0; t < NA; ++t) {
-      acc[t][0] = acc[t][0] > kFloor ? acc[t][0] : kFloor;
-      acc[t][1] = acc[t][1] > kFloor ? acc[t][1] : kFloor;
+    for (int t = 0; t < NA; ++t) {                 // floor (Q12); fmax(NaN, x) = x like the oracle
+      acc[t][0] = fmax(acc[t][0], kFloor);
+      acc[t][1] = fmax(acc[t][1], kFloor);
     }
     // neighbours: left of (t,q,0) is (t,q-1,1) [q>0] or (t-1,3,1) [q=0];
     //             right of (t,q,1) is (t,q+1,0) [q<3] or (t+1,0,0) [q=3]
-    const int srcL = q > 0 ? lane - 1 : lane + 3;
-    const int srcR = q < 3 ? lane + 1 : lane - 3;
     double up[NA], dn[NA];
 #pragma unroll
     for (int t = 0; t < NA; ++t) {
       up[t] = __shfl_sync(0xffffffffu, acc[t][1], srcL);
       dn[t] = __shfl_sync(0xffffffffu, acc[t][0], srcR);
     }
+    unsigned hit = 0;
 #pragma unroll
     for (int t = 0; t < NA; ++t) {
+      const double fl0 = q > 0 ? up[t] : (t > 0 ? up[t - 1] : acc[t][0]);
+      const double fr1 = q < 3 ? dn[t] : (t + 1 < NA ? dn[t + 1] : acc[t][1]);
+      hit |= (unsigned)(acc[t][0] < fl0 && acc[t][0] <= acc[t][1]) << (2 * t);
+      hit |= (unsigned)(acc[t][1] < acc[t][0] && acc[t][1] <= fr1) << (2 * t + 1);
+    }
+    const int b = (int)(g * 8) + r;
+    const bool frame_ok = b < B;
+    hit &= frame_ok ? dmask : 0u;
+    if (hit) {                                     // local maxima of P (rare): append candidates
+      do {
+        const int k = __ffs(hit) - 1;
+        hit &= hit - 1;
+        const int t = k >> 1, e = k & 1;
+        double f = 0.0;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int pos = 8 * t + 2 * q + e;
-        const int64_t i = base + pos;
-        const double f = acc[t][e];
-        double fl, fr;
-        if (e == 0) { fl = q > 0 ? up[t] : (t > 0 ? up[t - 1] : f); fr = acc[t][1]; }
-        else { fl = acc[t][0]; fr = q < 3 ? dn[t] : (t + 1 < NA ? dn[t + 1] : f); }
-        const bool inner = pos >= 1 && pos <= W - 2;
-        if (frame_ok && inner && i >= 1 && i <= L - 2 && f < fl && f <= fr) {
-          const int slot = atomicAdd(cnt + b, 1);
-          if (slot < cap) {
-            cidx[(size_t)b * cap + slot] = (int32_t)i;
-            cf[(size_t)b * cap + slot] = f;
-          }
+        for (int tt = 0; tt < NA; ++tt)
+          if (tt == t) f = e ? acc[tt][1] : acc[tt][0];
+        const int slot = atomicAdd(cnt + b, 1);
+        if (slot < cap) {
+          cidx[(size_t)b * cap + slot] = base + 8 * t + 2 * q + e;
+          cf[(size_t)b * cap + slot] = f;
         }
-        if (P && frame_ok && inner && i < L) P[(size_t)b * L + i] = to_p32(f);
+      } while (hit);
+    }
+    if (WRITE_P && frame_ok) {
+      float* Pb = P + (size_t)b * L + base + 2 * q;
+#pragma unroll
+      for (int t = 0; t < NA; ++t) {
+        if (omask & (1u << (2 * t))) Pb[8 * t] = to_p32(acc[t][0]);
+        if (omask & (1u << (2 * t + 1))) Pb[8 * t + 1] = to_p32(acc[t][1]);
       }
     }
   }
@@ -267,17 +296,22 @@ int64_t waves_chunk(int64_t cols, int64_t units, int64_t min_per_cta) {
   return per;
 }
 
-template <int M>
+template <int M, int NA>
 cudaError_t launch_scan_t(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
-  constexpr int W = ScanShape<M>::W;
+  constexpr int W = ScanShape<M, NA>::W;
   const int64_t nwb = (p->L + (W - 2) - 1) / (W - 2);           // warp blocks owning [0, L)
   const int64_t gx = (nwb + kScanWarps - 1) / kScanWarps;
   const int64_t ngroups = (B + 7) / 8;
   const int64_t per = waves_chunk(gx, ngroups, 8);
   const int64_t gy = (ngroups + per - 1) / per;
   count_launch();
-  scan_dmma_kernel<M><<<dim3((unsigned)gx, (unsigned)gy), kScanWarps * 32, 0, s>>>(
-      p->coef, B, per, p->dl, p->theta0, p->dtheta, p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
+  const dim3 grid((unsigned)gx, (unsigned)gy);
+  if (P)
+    scan_dmma_kernel<M, NA, true><<<grid, kScanWarps * 32, 0, s>>>(
+        p->coef, B, per, p->dl, p->theta0, p->dtheta, (int)p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
+  else
+    scan_dmma_kernel<M, NA, false><<<grid, kScanWarps * 32, 0, s>>>(
+        p->coef, B, per, p->dl, p->theta0, p->dtheta, (int)p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
   return cudaGetLastError();
 }
 
@@ -333,7 +367,7 @@ cudaError_t launch_coef(const doa_plan_s* p, const double* lam, const double* V,
 
 cudaError_t launch_scan(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
   switch (p->M) {
-#define DOA_SCAN_CASE(m) case m: return launch_scan_t<m>(p, B, P, s);
+#define DOA_SCAN_CASE(m) case m: return launch_scan_t<m, ScanShape<m>::NA>(p, B, P, s);
     DOA_SCAN_CASE(2) DOA_SCAN_CASE(3) DOA_SCAN_CASE(4) DOA_SCAN_CASE(5) DOA_SCAN_CASE(6) DOA_SCAN_CASE(7)
     DOA_SCAN_CASE(8) DOA_SCAN_CASE(9) DOA_SCAN_CASE(10) DOA_SCAN_CASE(11) DOA_SCAN_CASE(12) DOA_SCAN_CASE(13)
     DOA_SCAN_CASE(14) DOA_SCAN_CASE(15) DOA_SCAN_CASE(16) DOA_SCAN_CASE(17) DOA_SCAN_CASE(18) DOA_SCAN_CASE(19)

@@ -50,6 +50,32 @@ __global__ void dmma_k(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+// DMMA and DFMA interleaved: do the tensor-DMMA subpipe and the FP64 FMA pipe add up?
+template<int ND, int NF>
+__global__ void mix_k(double* out, int iters, double x, double y) {
+  double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+  double c[4][2];
+  double f[NF];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) { c[k][0] = 0; c[k][1] = 0; }
+#pragma unroll
+  for (int k = 0; k < NF; ++k) f[k] = k + threadIdx.x;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < ND; ++k)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[k & 3][0]), "+d"(c[k & 3][1]) : "d"(a), "d"(b));
+#pragma unroll
+    for (int k = 0; k < NF; ++k) f[k] = fma(f[k], x, y);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) s += c[k][0] + c[k][1];
+#pragma unroll
+  for (int k = 0; k < NF; ++k) s += f[k];
+  if (s == 12345.678) out[0] = s;
+}
+
 __global__ void cvt_k(double* out, int iters, const float* in) {
   float x[8];
 #pragma unroll
@@ -90,6 +116,10 @@ int main() {
   run("ffma_ch8", [&]{ ffma_k<<<blocks, threads>>>(f, iters, 0.999f, 1e-3f); }, 16.0);
   // DMMA m8n8k4: 8*8*4 FMA per warp per instr = 256 FMA = 512 flop per warp -> 16 flop per thread per mma
   run("dmma_m8n8k4 x4 (flop)", [&]{ dmma_k<<<blocks, threads>>>(d, iters); }, 4 * 16.0);
+  // flops per thread per iter: DMMA 16 flop/thread each, DFMA 2 flop each
+  run("mix 4 DMMA + 16 DFMA", [&]{ mix_k<4, 16><<<blocks, threads>>>(d, iters, 0.999, 1e-3); }, 4 * 16.0 + 16 * 2.0);
+  run("mix 4 DMMA + 32 DFMA", [&]{ mix_k<4, 32><<<blocks, threads>>>(d, iters, 0.999, 1e-3); }, 4 * 16.0 + 32 * 2.0);
+  run("mix 4 DMMA + 8 DFMA", [&]{ mix_k<4, 8><<<blocks, threads>>>(d, iters, 0.999, 1e-3); }, 4 * 16.0 + 8 * 2.0);
   run("cvt_f32_f64 x8 (ops)", [&]{ cvt_k<<<blocks, threads>>>(d, iters, f); }, 8.0);
   return 0;
 }
