@@ -193,7 +193,7 @@ def main():
 
     ws, rank, local = dist_env()
     B = args.frames or cfg.B
-    frames = range(rank * B, (rank + 1) * B)
+    frames = range(rank * B, (rank + 1) * B)      # == dist.weak_range(B, rank): own batch per rank
     # generate this rank's frames BEFORE touching CUDA (the generator forks worker processes)
     from synth import generate
     t0 = time.perf_counter()
@@ -208,6 +208,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     import paper_2007_14135_b200 as doa
     from paper_2007_14135_b200 import binding as bd
+    from paper_2007_14135_b200 import dist as pdist
 
     Xh = torch.from_numpy(Xh_np).pin_memory()
     del Xh_np
@@ -251,11 +252,8 @@ def main():
             bd.doa_peaks(p.h, B, idx[a], val[a], npk[a], info[a], s)
             launches += bd.doa_last_launch_count()
         if ws > 1:
-            packed[:, :, :D] = idx
-            packed[:, :, D:2 * D] = val.view(torch.int32)
-            packed[:, :, 2 * D] = npk
-            packed[:, :, 2 * D + 1] = info
-            dist.all_gather_into_tensor(gathered, packed)
+            pdist.pack_peaks(idx, val, npk, info, out=packed)
+            pdist.gather_peaks(packed, out=gathered)
         return launches
 
     for _ in range(max(3, args.warmup)):

@@ -1,25 +1,31 @@
-// S2 for M <= 16: batched Hermitian Jacobi eigendecomposition, one warp per matrix, with the
-// eigenvector matrix resident in registers.  (Table 2 Step-2 `jsvd`; Q3.)
+// S2 for M <= 16: batched Hermitian Jacobi eigendecomposition, one warp per matrix.
+// (Table 2 Step-2 `jsvd`; read as the Hermitian eigendecomposition, Q3.)
 //
-// Ordering: parallel cyclic Jacobi, circle-method round robin on n = 16 indices (M < 16 is padded
-// with decoupled zero indices that no rotation ever touches).  The 8 disjoint pairs of a round
-// always sit in fixed SLOTS (0,1), (2,3), ..., (14,15); after each round the slot contents move by
-// the fixed "caterpillar" permutation pi (slot 0 fixed, the other 15 slots rotate along one circle),
-// so every pair of indices meets exactly once per 15-round sweep.  sigma[slot] = logical index.
+// Ordering: parallel cyclic Jacobi with the circle-method round robin on n = 16 indices (M < 16
+// is padded with decoupled zero indices that no rotation ever touches).  The 8 disjoint pairs of a
+// round always sit in fixed SLOTS (0,1), (2,3), ..., (14,15); after each round every index moves
+// to the next slot of the "caterpillar" permutation pi (slot 0 fixed, slots 1..15 rotate along
+// one 15-cycle), so every pair of indices meets exactly once per 15-round sweep and, because
+// pi^15 = id, slots coincide with the original indices again at every sweep boundary.
 //
-//   A (Hermitian, logical indexing, upper triangle only) lives in shared memory.  Per round:
-//     phase 1  lanes 0..7   : rotation of slot-pair k from (a_xx, a_yy, a_xy), x = sigma[2k],
-//                             y = sigma[2k+1]; the 2x2 diagonal block gets its closed form
-//                             (a_xx - t|a_xy|, a_yy + t|a_xy|, 0) (Golub & Van Loan sym.schur2).
+//   A (Hermitian, physical slot order, upper triangle only) lives in shared memory,
+//   double-buffered: each round reads buffer `cur` and writes every upper element of buffer `nxt`
+//   at its PERMUTED position (pi(i), pi(j)) (conjugated when the permutation swaps the triangle),
+//   so the permutation costs only static per-lane store addresses.  The smem layout
+//   (i, j) -> i*19 + (j ^ (i/2)) and the lane -> block order below minimise bank conflicts of the
+//   block reads / permuted writes (searched offline: 48 wavefronts per round vs 104 row-major).
+//     phase 1  lanes 0..7   : rotation of slot pair k from (a_xx, a_yy, a_xy) and the closed-form
+//                             2x2 diagonal block (a_xx - t|a_xy|, a_yy + t|a_xy|, 0)
+//                             (Golub & Van Loan sym.schur2 after the phase rotation).
 //     phase 2  lanes 0..27  : one off-diagonal 2x2 block (slot pairs r < s): B <- J_r^H B J_s.
-//              all 32 lanes : V <- V J on registers.
+//              all 32 lanes : V <- V J in registers.
 //   V lives in registers: lane (row i = lane % 16, half h = lane / 16) holds V[i][slots 8h..8h+7];
-//     its 4 slot pairs are local, and pi moves only two slots across halves per round (one
-//     complex shuffle).
-// Rotations: J = diag(1, e) [[c, s], [-s, c]], e = conj(a_xy)/|a_xy|, tau = (a_yy - a_xx)/(2|a_xy|),
-// t = sign(tau)/(|tau| + sqrt(1 + tau^2)), c = 1/sqrt(1 + t^2), s = t c; skipped when a_xy == 0.
+//   its four slot pairs are local and pi moves only two slots across the halves per round (one
+//   complex shuffle); the rest of pi is register renaming.
+// Rotation: J = diag(1, e) [[c, s], [-s, c]], e = conj(a_xy)/|a_xy|, tau = (a_yy - a_xx)/(2|a_xy|),
+// t = sign(tau)/(|tau| + sqrt(1 + tau^2)), c = 1/sqrt(1 + t^2), s = t c; identity when a_xy == 0.
 // Stop rule at the start of every sweep: off(A) = sqrt(sum_{i != j} |a_ij|^2) <= 10 eps ||R||_F,
-// at most 30 sweeps (Q15).  Eigenvalues ascending, ties by logical index (Q2).
+// at most 30 sweeps (Q15).  Eigenvalues ascending, ties by index (Q2).
 #include <cfloat>
 
 #include "doa_internal.cuh"
@@ -28,8 +34,17 @@ namespace doa {
 namespace {
 
 constexpr int kN = 16;            // padded order
-constexpr int kLd = 17;           // smem row stride (double2)
+constexpr int kLd = 19;           // smem row stride (double2)
 constexpr int kEigWarps = 4;
+#ifndef DOA_EIG_MINB
+#define DOA_EIG_MINB 4
+#endif
+
+__device__ __forceinline__ int aidx(int i, int j) { return i * kLd + (j ^ (i >> 1)); }
+
+// lane -> off-diagonal slot-pair block (index into the row-major list of r < s pairs)
+__device__ constexpr int kBlockOrder[28] = {7, 1, 25, 2, 24, 17, 20, 18, 12, 19, 13, 5, 21, 4,
+                                             22, 3, 14, 8, 9, 11, 23, 26, 27, 16, 15, 10, 0, 6};
 
 struct Prm {
   double c, s, er, ei;
@@ -41,17 +56,6 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
-// canonical Hermitian access: element (i, j) of the logical matrix, stored at [min][max]
-__device__ __forceinline__ double2 aget(const double2* A, int i, int j) {
-  if (i <= j) return A[i * kLd + j];
-  const double2 v = A[j * kLd + i];
-  return make_double2(v.x, -v.y);
-}
-__device__ __forceinline__ void aset(double2* A, int i, int j, double2 v) {
-  if (i <= j) A[i * kLd + j] = v;
-  else A[j * kLd + i] = make_double2(v.x, -v.y);
-}
-
 // caterpillar: next slot of slot s
 __device__ __forceinline__ int cat_next(int s) {
   if (s == 0) return 0;
@@ -60,126 +64,161 @@ __device__ __forceinline__ int cat_next(int s) {
   return (s & 1) ? s - 2 : s + 2;
 }
 
-__global__ void __launch_bounds__(kEigWarps * 32) eig16_kernel(const double2* __restrict__ R, int64_t B, int M,
-                                                             double* __restrict__ lam_out,
-                                                             double2* __restrict__ V_out,
-                                                             int32_t* __restrict__ info) {
-  __shared__ double2 As[kEigWarps][kN * kLd];
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {   // conj(a) * b
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+
+__global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(const double2* __restrict__ R,
+                                                                             int64_t B, int M,
+                                                                             double* __restrict__ lam_out,
+                                                                             double2* __restrict__ V_out,
+                                                                             int32_t* __restrict__ info) {
+  __shared__ double2 As[kEigWarps][2][kN * kLd];
   __shared__ Prm prm[kEigWarps][kN / 2];
-  __shared__ int sig[kEigWarps][2][kN];
   __shared__ int rank_s[kEigWarps][kN];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t b = (int64_t)blockIdx.x * kEigWarps + warp;
   if (b >= B) return;
-  double2* A = As[warp];
   const double2* Rb = R + (size_t)b * M * M;
 
   // load the upper triangle (zero-padded to 16) and ||R||_F
   double nrm = 0.0;
-  for (int e = lane; e < kN * kN; e += 32) {
-    const int i = e >> 4, j = e & 15;
-    if (i > j) continue;
-    double2 v = make_double2(0.0, 0.0);
-    if (j < M) v = Rb[(size_t)i * M + j];
-    if (i == j) v.y = 0.0;
-    A[i * kLd + j] = v;
-    nrm += (i == j ? 1.0 : 2.0) * (v.x * v.x + v.y * v.y);
+  {
+    double2* A0 = As[warp][0];
+    for (int e = lane; e < kN * kN; e += 32) {
+      const int i = e >> 4, j = e & 15;
+      if (i > j) continue;
+      double2 v = make_double2(0.0, 0.0);
+      if (j < M) v = Rb[(size_t)i * M + j];
+      if (i == j) v.y = 0.0;
+      A0[aidx(i, j)] = v;
+      nrm += (i == j ? 1.0 : 2.0) * (v.x * v.x + v.y * v.y);
+    }
   }
-  if (lane < kN) sig[warp][0][lane] = lane;
   nrm = sqrt(wsum(nrm));
   const double tol = 10.0 * DBL_EPSILON * nrm;
 
-  // V registers: row vi, slots 8h..8h+7 (initially slot == logical index, V = I)
+  // V registers: row vi, slots 8h..8h+7 (V = I)
   const int vi = lane & 15, h = lane >> 4;
   double2 v[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) v[k] = make_double2(vi == 8 * h + k ? 1.0 : 0.0, 0.0);
 
-  // this lane's off-diagonal slot-pair block (rb < sb), lanes 0..27
-  int rb = 0, sb = 0;
+  // static per-lane geometry.  Off-diagonal block (rb < sb) for lanes 0..27.
+  int rb = 0, sb = 1;
   {
-    int l = lane < 28 ? lane : 0;
+    int l = lane < 28 ? kBlockOrder[lane] : 0;
     for (int r = 0; r < 8; ++r) {
       const int cntr = 7 - r;
       if (l < cntr) { rb = r; sb = r + 1 + l; break; }
       l -= cntr;
     }
   }
+  const int i0 = 2 * rb, i1 = 2 * rb + 1, j0 = 2 * sb, j1 = 2 * sb + 1;
+  const int rd00 = aidx(i0, j0), rd01 = aidx(i0, j1), rd10 = aidx(i1, j0), rd11 = aidx(i1, j1);
+  int wr[4];
+  double sg[4];                         // +1: store as is, -1: the permutation swapped the triangle
+  {
+    const int pr[2] = {cat_next(i0), cat_next(i1)}, pc[2] = {cat_next(j0), cat_next(j1)};
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int x = pr[a], y = pc[c];
+        wr[2 * a + c] = x < y ? aidx(x, y) : aidx(y, x);
+        sg[2 * a + c] = x < y ? 1.0 : -1.0;
+      }
+  }
+  // phase-1 geometry (lanes 0..7): pair k = lane
+  const int kx = 2 * (lane & 7), ky = kx + 1, px = cat_next(kx), py = cat_next(ky);
+  const int rxy = aidx(kx, ky), rxx = aidx(kx, kx), ryy = aidx(ky, ky);
+  const int wxx = aidx(px, px), wyy = aidx(py, py), wxy = px < py ? aidx(px, py) : aidx(py, px);
   __syncwarp();
 
   int flag = 0;
   int cur = 0;
   for (int sweep = 0;; ++sweep) {
-    double off = 0.0;
-    for (int e = lane; e < kN * kN; e += 32) {
-      const int i = e >> 4, j = e & 15;
-      if (i < j) { const double2 a = A[i * kLd + j]; off += a.x * a.x + a.y * a.y; }
+    {
+      const double2* A = As[warp][cur];
+      double off = 0.0;
+      for (int e = lane; e < kN * kN; e += 32) {
+        const int i = e >> 4, j = e & 15;
+        if (i < j) { const double2 a = A[aidx(i, j)]; off += a.x * a.x + a.y * a.y; }
+      }
+      off = sqrt(2.0 * wsum(off));
+      if (off <= tol) break;
+      if (sweep == kMaxSweeps) { flag |= DOA_INFO_NOCONV; break; }
     }
-    off = sqrt(2.0 * wsum(off));
-    if (off <= tol) break;
-    if (sweep == kMaxSweeps) { flag |= DOA_INFO_NOCONV; break; }
     for (int rnd = 0; rnd < kN - 1; ++rnd) {
-      const int* sc = sig[warp][cur];
-      // ---- phase 1: rotation parameters + closed-form diagonal blocks
+      const double2* A = As[warp][cur];
+      double2* An = As[warp][cur ^ 1];
+      // ---- phase 1: rotation of slot pair k = lane (lanes 0..7) + closed-form diagonal block
       if (lane < 8) {
-        const int x = sc[2 * lane], y = sc[2 * lane + 1];
-        const double2 axy = aget(A, x, y);
+        const double2 axy = A[rxy];
+        const double axx = A[rxx].x, ayy = A[ryy].x;
         const double r2 = axy.x * axy.x + axy.y * axy.y;
         Prm p;
+        double nxx = axx, nyy = ayy;
         if (r2 == 0.0) {
           p.c = 1.0; p.s = 0.0; p.er = 1.0; p.ei = 0.0;
         } else {
-          const double axx = A[x * kLd + x].x, ayy = A[y * kLd + y].x;
-          const double rr = sqrt(r2);
-          p.er = axy.x / rr;
-          p.ei = -axy.y / rr;
-          const double tau = (ayy - axx) / (2.0 * rr);
-          const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-          p.c = 1.0 / sqrt(1.0 + t * t);
+          // reciprocal square roots (MUFU seed + Newton, ~1 ulp) instead of IEEE div/sqrt
+          const double ir = rsqrt(r2);                        // 1/|a_xy|
+          const double rr = r2 * ir;                          // |a_xy|
+          p.er = axy.x * ir;
+          p.ei = -axy.y * ir;
+          const double tau = (ayy - axx) * (0.5 * ir);
+          const double at = fabs(tau);
+          double t;
+          if (at > 1e150) {
+            t = 0.5 / at;                                     // 1/(|tau| + sqrt(1 + tau^2)) -> 1/(2|tau|)
+          } else {
+            const double w = fma(at, at, 1.0);
+            t = __drcp_rn(at + w * rsqrt(w));
+          }
+          if (tau < 0.0) t = -t;
+          p.c = rsqrt(fma(t, t, 1.0));
           p.s = t * p.c;
-          A[x * kLd + x].x = axx - t * rr;
-          A[y * kLd + y].x = ayy + t * rr;
-          aset(A, x, y, make_double2(0.0, 0.0));
+          nxx = axx - t * rr;
+          nyy = ayy + t * rr;
         }
         prm[warp][lane] = p;
+        An[wxx] = make_double2(nxx, 0.0);
+        An[wyy] = make_double2(nyy, 0.0);
+        An[wxy] = make_double2(0.0, 0.0);
       }
       __syncwarp();
-      // ---- phase 2a: off-diagonal block (rb, sb): B <- J_r^H B J_s
+      // ---- phase 2a: off-diagonal block (rb, sb): B <- J_r^H B J_s, stored permuted
       if (lane < 28) {
         const Prm pr = prm[warp][rb], ps = prm[warp][sb];
-        const int xr = sc[2 * rb], yr = sc[2 * rb + 1], xs = sc[2 * sb], ys = sc[2 * sb + 1];
-        double2 b00 = aget(A, xr, xs), b01 = aget(A, xr, ys), b10 = aget(A, yr, xs), b11 = aget(A, yr, ys);
-        // columns: c0' = c b0 - s (e b1), c1' = s b0 + c (e b1), with e = e_s
-        {
-          double2 t0 = make_double2(ps.er * b01.x - ps.ei * b01.y, ps.er * b01.y + ps.ei * b01.x);
-          double2 t1 = make_double2(ps.er * b11.x - ps.ei * b11.y, ps.er * b11.y + ps.ei * b11.x);
-          const double2 n00 = make_double2(ps.c * b00.x - ps.s * t0.x, ps.c * b00.y - ps.s * t0.y);
-          const double2 n01 = make_double2(ps.s * b00.x + ps.c * t0.x, ps.s * b00.y + ps.c * t0.y);
-          const double2 n10 = make_double2(ps.c * b10.x - ps.s * t1.x, ps.c * b10.y - ps.s * t1.y);
-          const double2 n11 = make_double2(ps.s * b10.x + ps.c * t1.x, ps.s * b10.y + ps.c * t1.y);
-          b00 = n00; b01 = n01; b10 = n10; b11 = n11;
-        }
-        // rows: r0' = c r0 - s (conj(e) r1), r1' = s r0 + c (conj(e) r1), with e = e_r
-        {
-          const double2 t0 = make_double2(pr.er * b10.x + pr.ei * b10.y, pr.er * b10.y - pr.ei * b10.x);
-          const double2 t1 = make_double2(pr.er * b11.x + pr.ei * b11.y, pr.er * b11.y - pr.ei * b11.x);
-          aset(A, xr, xs, make_double2(pr.c * b00.x - pr.s * t0.x, pr.c * b00.y - pr.s * t0.y));
-          aset(A, xr, ys, make_double2(pr.c * b01.x - pr.s * t1.x, pr.c * b01.y - pr.s * t1.y));
-          aset(A, yr, xs, make_double2(pr.s * b00.x + pr.c * t0.x, pr.s * b00.y + pr.c * t0.y));
-          aset(A, yr, ys, make_double2(pr.s * b01.x + pr.c * t1.x, pr.s * b01.y + pr.c * t1.y));
-        }
+        const double2 b00 = A[rd00], b01 = A[rd01], b10 = A[rd10], b11 = A[rd11];
+        const double2 es = make_double2(ps.er, ps.ei), er = make_double2(pr.er, pr.ei);
+        // columns (J_s): c0' = c b0 - s (e b1), c1' = s b0 + c (e b1)
+        const double2 t0 = cmul(es, b01), t1 = cmul(es, b11);
+        const double2 n00 = make_double2(ps.c * b00.x - ps.s * t0.x, ps.c * b00.y - ps.s * t0.y);
+        const double2 n01 = make_double2(ps.s * b00.x + ps.c * t0.x, ps.s * b00.y + ps.c * t0.y);
+        const double2 n10 = make_double2(ps.c * b10.x - ps.s * t1.x, ps.c * b10.y - ps.s * t1.y);
+        const double2 n11 = make_double2(ps.s * b10.x + ps.c * t1.x, ps.s * b10.y + ps.c * t1.y);
+        // rows (J_r^H): r0' = c r0 - s (conj(e) r1), r1' = s r0 + c (conj(e) r1)
+        const double2 u0 = cmulc(er, n10), u1 = cmulc(er, n11);
+        An[wr[0]] = make_double2(pr.c * n00.x - pr.s * u0.x, sg[0] * (pr.c * n00.y - pr.s * u0.y));
+        An[wr[1]] = make_double2(pr.c * n01.x - pr.s * u1.x, sg[1] * (pr.c * n01.y - pr.s * u1.y));
+        An[wr[2]] = make_double2(pr.s * n00.x + pr.c * u0.x, sg[2] * (pr.s * n00.y + pr.c * u0.y));
+        An[wr[3]] = make_double2(pr.s * n01.x + pr.c * u1.x, sg[3] * (pr.s * n01.y + pr.c * u1.y));
       }
-      // ---- phase 2b: V <- V J for this lane's four slot pairs (registers)
+      // ---- phase 2b: V <- V J on this lane's four slot pairs (registers)
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const Prm p = prm[warp][4 * h + kk];
         const double2 vx = v[2 * kk], vy = v[2 * kk + 1];
-        const double2 t = make_double2(p.er * vy.x - p.ei * vy.y, p.er * vy.y + p.ei * vy.x);
+        const double2 t = cmul(make_double2(p.er, p.ei), vy);
         v[2 * kk] = make_double2(p.c * vx.x - p.s * t.x, p.c * vx.y - p.s * t.y);
         v[2 * kk + 1] = make_double2(p.s * vx.x + p.c * t.x, p.s * vx.y + p.c * t.y);
       }
-      // ---- caterpillar: slots move s -> pi(s) (sigma in smem, V in registers)
-      if (lane < kN) sig[warp][cur ^ 1][cat_next(lane)] = sc[lane];
+      // ---- caterpillar on V's column slots: s -> pi(s)
       {
         const double2 send = h ? v[1] : v[6];
         const double2 recv = make_double2(__shfl_xor_sync(0xffffffffu, send.x, 16),
@@ -199,13 +238,13 @@ __global__ void __launch_bounds__(kEigWarps * 32) eig16_kernel(const double2* __
     }
   }
 
-  // ascending stable sort of the logical diagonal, then scatter V's columns (slot -> logical)
-  const int* sc = sig[warp][cur];
+  // after whole sweeps slot == index (pi^15 = id): ascending stable sort of the diagonal
+  const double2* A = As[warp][cur];
   if (lane < M) {
-    const double li = A[lane * kLd + lane].x;
+    const double li = A[aidx(lane, lane)].x;
     int rk = 0;
     for (int j = 0; j < M; ++j) {
-      const double lj = A[j * kLd + j].x;
+      const double lj = A[aidx(j, j)].x;
       rk += (lj < li) || (lj == li && j < lane);
     }
     rank_s[warp][lane] = rk;
@@ -216,7 +255,7 @@ __global__ void __launch_bounds__(kEigWarps * 32) eig16_kernel(const double2* __
     double2* Vrow = V_out + (size_t)b * M * M + (size_t)vi * M;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int j = sc[8 * h + k];
+      const int j = 8 * h + k;
       if (j < M) Vrow[rank_s[warp][j]] = v[k];
     }
   }

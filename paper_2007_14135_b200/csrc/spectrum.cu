@@ -9,6 +9,7 @@
 // F[b][i] = sum_j coef[b][j] T[j][i] (Table 2 Step-5), K = 4S >= 2M-1, run on the FP64
 // tensor pipe (DMMA, mma.sync m8n8k4 f64) with the table resident in registers.
 #include <cfloat>
+#include <cstdlib>
 
 #include "doa_internal.cuh"
 
@@ -28,65 +29,96 @@ __device__ __forceinline__ float to_p32(double f) {
 //   MN : u = P_n e1 / (e1^H P_n e1), P_n e1 = sum_j e_j conj(e_j[0]) (Q5); p0 <= 100 eps: DEGENERATE.
 // Writes the coefficients in the scan's A-fragment layout (coef_index) and zeroes the frame's
 // candidate counter for the scan that follows.
-__global__ void __launch_bounds__(128) coef_kernel(const double* __restrict__ lam, const double2* __restrict__ V,
-                                                  int64_t B, int M, int D, int alg, double* __restrict__ coef,
-                                                  int32_t* __restrict__ cnt, int32_t* __restrict__ info) {
-  __shared__ double2 mn_w[4][kMaxM];
+// The frame's noise vectors are staged transposed in shared memory (U[j][p], coalesced global
+// reads of V's rows), so the lanes computing different lags k read consecutive addresses.  Lanes
+// are split into M lags x H = 32/M vector-slices (M <= 16: every lane busy); the H partial sums
+// of a lag are combined in a fixed order (deterministic).
+constexpr int kCoefWarps = 4;
+
+__global__ void __launch_bounds__(kCoefWarps * 32) coef_kernel(const double* __restrict__ lam,
+                                                              const double2* __restrict__ V, int64_t B, int M,
+                                                              int D, int alg, double* __restrict__ coef,
+                                                              int32_t* __restrict__ cnt, int32_t* __restrict__ info) {
+  extern __shared__ double2 csm[];                    // per warp: U[M][M+1], then part[32] (double2)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t b = (int64_t)blockIdx.x * 4 + warp;
+  const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (b >= B) return;
+  const int ld = M + 1;
+  double2* U = csm + (size_t)warp * (M * ld + 32);
+  double2* part = U + M * ld;
   const int S = ksteps(M);
   const double2* Vb = V + (size_t)b * M * M;
   const double* lb = lam + (size_t)b * M;
   const int K = M - D;
   int flag = 0;
-  int nv = 1;
-  if (alg == DOA_ALG_MUSIC || alg == DOA_ALG_EV) nv = K;
+  const int nload = (alg == DOA_ALG_PHD) ? 1 : K;      // columns needed
+  for (int e = lane; e < M * M; e += 32) {
+    const int p = e / M, j = e - (e / M) * M;
+    if (j < nload) U[j * ld + p] = Vb[e];
+  }
   double lfloor = 0.0;
   if (alg == DOA_ALG_EV) {
     lfloor = 100.0 * DBL_EPSILON * fmax(lb[M - 1], 0.0);
     for (int j = 0; j < K; ++j) if (lb[j] <= lfloor) flag |= DOA_INFO_DEGENERATE;
   }
+  __syncwarp();
+  int nv = (alg == DOA_ALG_MUSIC || alg == DOA_ALG_EV) ? K : 1;
   if (alg == DOA_ALG_MN) {
+    // w = P_n e1 / (e1^H P_n e1): P_n e1 = sum_j e_j conj(e_j[0]), e1^H P_n e1 = sum_j |e_j[0]|^2
     double p0 = 0.0;
-    for (int j = 0; j < K; ++j) { const double2 v = Vb[j]; p0 += v.x * v.x + v.y * v.y; }
+    for (int j = 0; j < K; ++j) { const double2 v = U[j * ld]; p0 += v.x * v.x + v.y * v.y; }
     const bool degen = !(p0 > 100.0 * DBL_EPSILON);
     if (degen) flag |= DOA_INFO_DEGENERATE;
     const double lp = degen ? 1.0 : 1.0 / p0;
-    for (int i = lane; i < M; i += 32) {
+    double2 wv[2];
+    for (int rep = 0, i = lane; rep < 2; ++rep, i += 32) {
       double pr = 0.0, pi = 0.0;
-      for (int j = 0; j < K; ++j) {
-        const double2 e = Vb[(size_t)i * M + j], e0 = Vb[j];
-        // e_j[i] * conj(e_j[0])
-        pr += e.x * e0.x + e.y * e0.y;
-        pi += e.y * e0.x - e.x * e0.y;
-      }
-      mn_w[warp][i] = degen ? make_double2(pr, pi) : make_double2(pr * lp, pi * lp);
+      if (i < M)
+        for (int j = 0; j < K; ++j) {
+          const double2 e = U[j * ld + i], e0 = U[j * ld];
+          pr += e.x * e0.x + e.y * e0.y;                 // e_j[i] * conj(e_j[0])
+          pi += e.y * e0.x - e.x * e0.y;
+        }
+      wv[rep] = degen ? make_double2(pr, pi) : make_double2(pr * lp, pi * lp);
     }
     __syncwarp();
+    for (int rep = 0, i = lane; rep < 2; ++rep, i += 32)
+      if (i < M) U[i] = wv[rep];                        // vector 0 <- w
+    __syncwarp();
   }
-  for (int k = lane; k < M; k += 32) {
+  const int H = M <= 16 ? 32 / M : 1;                  // vector slices per lag
+  for (int k0 = 0; k0 < M; k0 += 32) {                 // M = 64: two passes of 32 lags
+    const int k = k0 + (M <= 16 ? lane % M : lane);
+    const int hh = M <= 16 ? lane / M : 0;
     double cr = 0.0, ci = 0.0;
-    for (int j = 0; j < nv; ++j) {
-      double w = 1.0;
-      if (alg == DOA_ALG_EV) w = lb[j] <= lfloor ? (lfloor > 0.0 ? 1.0 / lfloor : 1.0) : 1.0 / lb[j];
-      double sr = 0.0, si = 0.0;
-      for (int p = 0; p + k < M; ++p) {
-        double2 x, y;
-        if (alg == DOA_ALG_MN) { x = mn_w[warp][p]; y = mn_w[warp][p + k]; }
-        else { x = Vb[(size_t)p * M + j]; y = Vb[(size_t)(p + k) * M + j]; }
-        // u[p] conj(u[p+k])
-        sr += x.x * y.x + x.y * y.y;
-        si += x.y * y.x - x.x * y.y;
+    if (k < M && hh < H) {
+      for (int j = hh; j < nv; j += H) {
+        const double2* u = U + j * ld;
+        double sr = 0.0, si = 0.0;
+        for (int p = 0; p + k < M; ++p) {
+          const double2 x = u[p], y = u[p + k];          // u[p] conj(u[p+k])
+          sr += x.x * y.x + x.y * y.y;
+          si += x.y * y.x - x.x * y.y;
+        }
+        const double w = (alg != DOA_ALG_EV) ? 1.0
+                         : (lb[j] <= lfloor ? (lfloor > 0.0 ? 1.0 / lfloor : 1.0) : 1.0 / lb[j]);
+        cr += w * sr;
+        ci += w * si;
       }
-      cr += w * sr;
-      ci += w * si;
     }
-    if (k == 0) coef[coef_index(b, 0, S)] = cr;
-    else {
-      coef[coef_index(b, k, S)] = 2.0 * cr;
-      coef[coef_index(b, M - 1 + k, S)] = 2.0 * ci;
+    part[lane] = make_double2(cr, ci);
+    __syncwarp();
+    if (lane < (M <= 16 ? M : 32) && k0 + lane < M) {
+      const int kk = k0 + lane;
+      double sr = 0.0, si = 0.0;
+      for (int h2 = 0; h2 < H; ++h2) { const double2 v = part[h2 * (M <= 16 ? M : 32) + lane]; sr += v.x; si += v.y; }
+      if (kk == 0) coef[coef_index(b, 0, S)] = sr;
+      else {
+        coef[coef_index(b, kk, S)] = 2.0 * sr;
+        coef[coef_index(b, M - 1 + kk, S)] = 2.0 * si;
+      }
     }
+    __syncwarp();
   }
   for (int j = 2 * M - 1 + lane; j < 4 * S; j += 32) coef[coef_index(b, j, S)] = 0.0;   // K padding
   if (lane == 0) {
@@ -127,6 +159,9 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 // peak test f_i < f_{i-1} && f_i <= f_{i+1} on interior indices (Q9/Q10), rare atomic append to
 // the frame's candidate list, optional fp32 P store.
 constexpr int kScanWarps = 4;
+#ifndef DOA_SCAN_NB
+#define DOA_SCAN_NB 2
+#endif
 #ifndef DOA_SCAN_MINB
 #define DOA_SCAN_MINB 2
 #endif
@@ -245,6 +280,134 @@ __global__ void __launch_bounds__(kScanWarps * 32, DOA_SCAN_MINB) scan_dmma_kern
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// S4-S6, CTA-shared table variant.  A CTA owns NB consecutive angle blocks of W = 8*NA angles
+// (each block: positions 0 and W-1 are halo, blocks advance by W-2) and a range of frame groups.
+// The table is generated ONCE per CTA into shared memory in B-fragment order
+// Ts[k][s][t][lane] = T_{4s + lane%4}(angle base_k + 8t + lane/4), so every B-fragment load is one
+// conflict-free 8-byte LDS per lane.  The CTA's 8 warps stream disjoint frame groups (warp w takes
+// g0 + w, g0 + w + 8, ...): per group one coalesced A-fragment load per k-step (reused for all NB
+// blocks), then per block S x NA DMMAs and the fused epilogue.  With ~100 registers per thread,
+// 16 warps per SM keep the DMMA pipe fed while other warps run their epilogues.
+constexpr int kCtaWarps = 8;
+constexpr long long kInfBits = 0x7FF0000000000000LL;        // bits of +inf
+constexpr long long kFloorBits = 0x01A56E1FC2F8F359LL;      // bits of 1e-300 (kFloor, Q12)
+#ifndef DOA_SCAN_CTA_MINB
+#define DOA_SCAN_CTA_MINB 3
+#endif
+
+template <int M, int NB, bool WRITE_P>
+__global__ void __launch_bounds__(kCtaWarps * 32, DOA_SCAN_CTA_MINB) scan_cta_kernel(const double* __restrict__ coef, int64_t B,
+                                                                   int64_t groups_per_cta, double dl,
+                                                                   double theta0, double dtheta, int L, int cap,
+                                                                   int32_t* __restrict__ cnt,
+                                                                   int32_t* __restrict__ cidx,
+                                                                   double* __restrict__ cf,
+                                                                   float* __restrict__ P) {
+  constexpr int S = ScanShape<M>::S, NA = ScanShape<M>::NA, W = ScanShape<M>::W;
+  extern __shared__ double Ts[];                                 // [NB][S][NA][32]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane & 3, r = lane >> 2;
+  const int blk0 = blockIdx.x * NB;
+  // table generation, all threads
+  for (int e = threadIdx.x; e < NB * S * NA * 32; e += kCtaWarps * 32) {
+    const int ln = e & 31, t = (e >> 5) % NA, s = (e / (32 * NA)) % S, k = e / (32 * NA * S);
+    const int i = (blk0 + k) * (W - 2) - 1 + 8 * t + (ln >> 2);
+    const int j = 4 * s + (ln & 3);
+    double v = (j == 0) ? 1.0 : 0.0;
+    if (i >= 0 && i < L) v = table_entry(j, M, grid_u(i, theta0, dtheta, dl));
+    Ts[e] = v;
+  }
+  __syncthreads();
+
+  const int srcL = q > 0 ? lane - 1 : lane + 3;
+  const int srcR = q < 3 ? lane + 1 : lane - 3;
+  const int64_t ngroups = (B + 7) / 8;
+  const int64_t g0 = (int64_t)blockIdx.y * groups_per_cta;
+  const int64_t g1 = (g0 + groups_per_cta < ngroups) ? g0 + groups_per_cta : ngroups;
+  for (int64_t g = g0 + warp; g < g1; g += kCtaWarps) {
+    double a[S];
+    const double* cg = coef + ((size_t)g * S) * 32 + lane;
+#pragma unroll
+    for (int s = 0; s < S; ++s) a[s] = __ldg(cg + s * 32);
+    const int b = (int)(g * 8) + r;
+    const bool frame_ok = b < B;
+#pragma unroll 1
+    for (int k = 0; k < NB; ++k) {
+      const int base = (blk0 + k) * (W - 2) - 1;
+      if (base + 1 >= L) break;                                  // warp-uniform
+      const double* Tk = Ts + (size_t)k * S * NA * 32 + lane;
+      double acc[NA][2];
+#pragma unroll
+      for (int t = 0; t < NA; ++t) { acc[t][0] = 0.0; acc[t][1] = 0.0; }
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int t = 0; t < NA; ++t) dmma_884(acc[t][0], acc[t][1], a[s], Tk[(s * NA + t) * 32]);
+      // Floor (Q12) and the peak test in the INTEGER domain: for non-negative doubles the IEEE
+      // bit patterns order exactly like the values, so the floored f are compared as signed
+      // 64-bit integers on the integer pipes while the FP64 pipe stays with the DMMAs.
+      // Negative values, -0, +0 and NaNs of either sign map to the floor like fmax(x, 1e-300).
+      long long fi[NA][2];
+#pragma unroll
+      for (int t = 0; t < NA; ++t)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          long long x = __double_as_longlong(acc[t][e]);
+          x = x > kInfBits ? kFloorBits : x;
+          fi[t][e] = x > kFloorBits ? x : kFloorBits;
+        }
+      long long up[NA], dn[NA];
+#pragma unroll
+      for (int t = 0; t < NA; ++t) {
+        up[t] = __shfl_sync(0xffffffffu, fi[t][1], srcL);
+        dn[t] = __shfl_sync(0xffffffffu, fi[t][0], srcR);
+      }
+      // lane pair (v0, v1) with outer neighbours L, R:  c = v1 < v0;
+      // v0 is a minimum iff !c && v0 < L;  v1 is a minimum iff c && v1 <= R   (Q10)
+      unsigned hit = 0;
+#pragma unroll
+      for (int t = 0; t < NA; ++t) {
+        const long long fl0 = q > 0 ? up[t] : (t > 0 ? up[t - 1] : fi[t][0]);
+        const long long fr1 = q < 3 ? dn[t] : (t + 1 < NA ? dn[t + 1] : fi[t][1]);
+        const bool c = fi[t][1] < fi[t][0];
+        hit |= (unsigned)(!c && fi[t][0] < fl0) << (2 * t);
+        hit |= (unsigned)(c && fi[t][1] <= fr1) << (2 * t + 1);
+      }
+      // decidable positions: block interior (pos 1..W-2) and grid interior (1..L-2)
+      if (!frame_ok) hit = 0;
+      if (hit) {
+        do {
+          const int kk = __ffs(hit) - 1;
+          hit &= hit - 1;
+          const int t = kk >> 1, e = kk & 1;
+          const int pos = 8 * t + 2 * q + e, i = base + pos;
+          if (pos < 1 || pos > W - 2 || i < 1 || i > L - 2) continue;
+          long long f = 0;
+#pragma unroll
+          for (int tt = 0; tt < NA; ++tt)
+            if (tt == t) f = e ? fi[tt][1] : fi[tt][0];
+          const int slot = atomicAdd(cnt + b, 1);
+          if (slot < cap) {
+            cidx[(size_t)b * cap + slot] = i;
+            cf[(size_t)b * cap + slot] = __longlong_as_double(f);
+          }
+        } while (hit);
+      }
+      if (WRITE_P && frame_ok) {
+        float* Pb = P + (size_t)b * L;
+#pragma unroll
+        for (int t = 0; t < NA; ++t)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int pos = 8 * t + 2 * q + e, i = base + pos;
+            if (pos >= 1 && pos <= W - 2 && i >= 0 && i < L) Pb[i] = to_p32(__longlong_as_double(fi[t][e]));
+          }
+      }
+    }
+  }
+}
+
 // Same contraction for any M <= 64 with the table in shared memory and plain DFMA (runtime M;
 // used for M > 32, where a register-resident table would spill).  Lanes own angles of a
 // 32-angle block with halo lanes 0 and 31 (stride 30).
@@ -296,8 +459,39 @@ int64_t waves_chunk(int64_t cols, int64_t units, int64_t min_per_cta) {
   return per;
 }
 
+template <int M, int NB>
+cudaError_t launch_scan_cta(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
+  constexpr int S = ScanShape<M>::S, NA = ScanShape<M>::NA, W = ScanShape<M>::W;
+  const int64_t nwb = (p->L + (W - 2) - 1) / (W - 2);           // angle blocks owning [0, L)
+  const int64_t gx = (nwb + NB - 1) / NB;
+  const int64_t ngroups = (B + 7) / 8;
+  // frame chunks: >= ~4 waves of 2 CTAs x 148 SMs, >= 64 groups (8 per warp) per CTA
+  int64_t per = (gx * ngroups) / (148 * 2 * 4);
+  if (per < 64) per = 64;
+  if (per > ngroups) per = ngroups;
+  const int64_t gy = (ngroups + per - 1) / per;
+  const size_t smem = (size_t)NB * S * NA * 32 * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(scan_cta_kernel<M, NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(scan_cta_kernel<M, NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  count_launch();
+  const dim3 grid((unsigned)gx, (unsigned)gy);
+  if (P)
+    scan_cta_kernel<M, NB, true><<<grid, kCtaWarps * 32, smem, s>>>(
+        p->coef, B, per, p->dl, p->theta0, p->dtheta, (int)p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
+  else
+    scan_cta_kernel<M, NB, false><<<grid, kCtaWarps * 32, smem, s>>>(
+        p->coef, B, per, p->dl, p->theta0, p->dtheta, (int)p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
+  return cudaGetLastError();
+}
+
 template <int M, int NA>
 cudaError_t launch_scan_t(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
+  static const bool warp_variant = getenv("DOA_SCAN_WARP") != nullptr;   // A/B switch for tuning only
+  if (!warp_variant) return launch_scan_cta<M, DOA_SCAN_NB>(p, B, P, s);
   constexpr int W = ScanShape<M, NA>::W;
   const int64_t nwb = (p->L + (W - 2) - 1) / (W - 2);           // warp blocks owning [0, L)
   const int64_t gx = (nwb + kScanWarps - 1) / kScanWarps;
@@ -359,9 +553,18 @@ __global__ void __launch_bounds__(128) select_kernel(int64_t B, int D, int cap, 
 
 cudaError_t launch_coef(const doa_plan_s* p, const double* lam, const double* V, int64_t B, int32_t* info,
                         cudaStream_t s) {
+  const int M = p->M;
+  const int wpc = M <= 32 ? kCoefWarps : 2;
+  const size_t smem = (size_t)wpc * (M * (M + 1) + 32) * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(coef_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(2 * (kMaxM * (kMaxM + 1) + 32) * sizeof(double2)));
+    attr = true;
+  }
   count_launch();
-  coef_kernel<<<(unsigned)((B + 3) / 4), 128, 0, s>>>(lam, reinterpret_cast<const double2*>(V), B, p->M, p->D,
-                                                       p->alg, p->coef, p->cnt, info);
+  coef_kernel<<<(unsigned)((B + wpc - 1) / wpc), wpc * 32, smem, s>>>(lam, reinterpret_cast<const double2*>(V), B, M,
+                                                                       p->D, p->alg, p->coef, p->cnt, info);
   return cudaGetLastError();
 }
 
