@@ -290,9 +290,17 @@ def main():
     pk = peaks_json()
     fp64_peak = 148 * 64 * 2 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12   # TFLOP/s, guide unit counts
     achieved = scan_flops / (spec_ms / 1e3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath) and cfg.name == "c4":
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("scan", {}).get("traffic_bytes")
     roofline = {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp64_peak, "traffic": None,
-                "kernel": "doa_spectrum (coef_kernel + scan_kernel<16>), fp64 DFMA pipe",
+                "frac": achieved / fp64_peak, "traffic": traffic,
+                "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one scan launch, ncu --set full "
+                                  "(profiles/traffic.json); algorithmic operand bytes per launch: coef 16.8 MB",
+                "kernel": "doa_spectrum = coef_kernel + scan kernel (FP64 DMMA mma.sync m8n8k4); events "
+                          "bracket both, so the scan's own fraction is higher",
                 "kernel_ms": spec_ms, "share_of_step": spec_ms * len(ALGS) / ms_step,
                 "peak_source": "148 SMs x 64 FP64 lanes x 2 flop x sm_max_mhz (guide unit counts; "
                                "measured DMMA 37.18 / DFMA 34.19 TFLOP/s in profiles/fp64_peaks_r01.txt)"}

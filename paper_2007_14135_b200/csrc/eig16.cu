@@ -152,43 +152,42 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
       if (off <= tol) break;
       if (sweep == kMaxSweeps) { flag |= DOA_INFO_NOCONV; break; }
     }
+#if DOA_EIG_UNROLL
+#pragma unroll
+#else
+#pragma unroll 1
+#endif
     for (int rnd = 0; rnd < kN - 1; ++rnd) {
       const double2* A = As[warp][cur];
       double2* An = As[warp][cur ^ 1];
-      // ---- phase 1: rotation of slot pair k = lane (lanes 0..7) + closed-form diagonal block
-      if (lane < 8) {
+      // ---- phase 1: rotation of slot pair k = lane & 7 + closed-form diagonal block.  Computed
+      // branch-free by all lanes (lanes 8..31 duplicate lanes 0..7); only lanes 0..7 store.
+      // Reciprocal square roots (MUFU seed + Newton, ~1 ulp) replace IEEE div/sqrt.
+      {
         const double2 axy = A[rxy];
         const double axx = A[rxx].x, ayy = A[ryy].x;
         const double r2 = axy.x * axy.x + axy.y * axy.y;
+        const bool rot = r2 != 0.0;                           // a_xy == 0: identity rotation
+        const double ir = rsqrt(rot ? r2 : 1.0);              // 1/|a_xy|
+        const double rr = r2 * ir;                            // |a_xy|
+        const double tau = (ayy - axx) * (0.5 * ir);
+        const double at = fabs(tau);
+        const double atc = fmin(at, 1e150);
+        const double w = fma(atc, atc, 1.0);
+        // 1/(|tau| + sqrt(1 + tau^2)); -> 1/(2|tau|) once tau^2 would overflow
+        double t = __drcp_rn(at > 1e150 ? 2.0 * at : atc + w * rsqrt(w));
+        t = rot ? (tau < 0.0 ? -t : t) : 0.0;
         Prm p;
-        double nxx = axx, nyy = ayy;
-        if (r2 == 0.0) {
-          p.c = 1.0; p.s = 0.0; p.er = 1.0; p.ei = 0.0;
-        } else {
-          // reciprocal square roots (MUFU seed + Newton, ~1 ulp) instead of IEEE div/sqrt
-          const double ir = rsqrt(r2);                        // 1/|a_xy|
-          const double rr = r2 * ir;                          // |a_xy|
-          p.er = axy.x * ir;
-          p.ei = -axy.y * ir;
-          const double tau = (ayy - axx) * (0.5 * ir);
-          const double at = fabs(tau);
-          double t;
-          if (at > 1e150) {
-            t = 0.5 / at;                                     // 1/(|tau| + sqrt(1 + tau^2)) -> 1/(2|tau|)
-          } else {
-            const double w = fma(at, at, 1.0);
-            t = __drcp_rn(at + w * rsqrt(w));
-          }
-          if (tau < 0.0) t = -t;
-          p.c = rsqrt(fma(t, t, 1.0));
-          p.s = t * p.c;
-          nxx = axx - t * rr;
-          nyy = ayy + t * rr;
+        p.c = rot ? rsqrt(fma(t, t, 1.0)) : 1.0;
+        p.s = t * p.c;
+        p.er = rot ? axy.x * ir : 1.0;
+        p.ei = rot ? -axy.y * ir : 0.0;
+        if (lane < 8) {
+          prm[warp][lane] = p;
+          An[wxx] = make_double2(axx - t * rr, 0.0);
+          An[wyy] = make_double2(ayy + t * rr, 0.0);
+          An[wxy] = make_double2(0.0, 0.0);
         }
-        prm[warp][lane] = p;
-        An[wxx] = make_double2(nxx, 0.0);
-        An[wyy] = make_double2(nyy, 0.0);
-        An[wxy] = make_double2(0.0, 0.0);
       }
       __syncwarp();
       // ---- phase 2a: off-diagonal block (rb, sb): B <- J_r^H B J_s, stored permuted

@@ -7,9 +7,8 @@
 // Each (frame, angle) then costs 2(M-1) fp64 FMAs against a per-angle table
 // T(psi) = (1, cos k psi, sin k psi) shared by every frame — the scan is the real contraction
 // F[b][i] = sum_j coef[b][j] T[j][i] (Table 2 Step-5), K = 4S >= 2M-1, run on the FP64
-// tensor pipe (DMMA, mma.sync m8n8k4 f64) with the table resident in registers.
+// tensor pipe (DMMA, mma.sync m8n8k4 f64) with the table staged once per CTA in shared memory.
 #include <cfloat>
-#include <cstdlib>
 
 #include "doa_internal.cuh"
 
@@ -148,241 +147,143 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 }
 
 // ---------------------------------------------------------------------------------------------
-// S4-S6 on the FP64 tensor pipe.  A warp owns a block of W = 8*NA consecutive grid angles
-// (positions 0 and W-1 are halo; warp blocks advance by W-2 so every interior angle is decided
-// by exactly one lane) and a range of frame groups (8 frames each).
-//   B-fragments (the steering table): lane holds T_{4s + lane%4}(angle 8t + lane/4), s < S,
-//     t < NA — generated once per warp with fp64 sincospi and kept in registers.
-//   A-fragments (coefficients): coef[8g + lane/4][4s + lane%4], one coalesced 8-byte load per s.
-//   D (8 frames x 8 angles per t): lane holds frame lane/4, angles 8t + 2(lane%4) + {0,1}.
-// Epilogue per group: floor (Q12), neighbour values by shuffles inside each 4-lane frame row,
-// peak test f_i < f_{i-1} && f_i <= f_{i+1} on interior indices (Q9/Q10), rare atomic append to
-// the frame's candidate list, optional fp32 P store.
-constexpr int kScanWarps = 4;
-#ifndef DOA_SCAN_NB
-#define DOA_SCAN_NB 2
-#endif
-#ifndef DOA_SCAN_MINB
-#define DOA_SCAN_MINB 2
-#endif
-
-template <int M, int NA_ = 0>
-struct ScanShape {
-  static constexpr int S = (2 * M + 3) / 4;                 // k-steps of 4
-  static constexpr int NA_default = (64 / S) < 8 ? (64 / S) : 8;
-  static constexpr int NA = NA_ > 0 ? NA_ : NA_default;     // 8-angle tiles per warp
-  static constexpr int W = 8 * NA;                           // angles per warp block (incl. 2 halo)
-};
-
-template <int M, int NA, bool WRITE_P>
-__global__ void __launch_bounds__(kScanWarps * 32, DOA_SCAN_MINB) scan_dmma_kernel(const double* __restrict__ coef, int64_t B,
-                                                                   int64_t groups_per_cta, double dl,
-                                                                   double theta0, double dtheta, int L,
-                                                                   int cap, int32_t* __restrict__ cnt,
-                                                                   int32_t* __restrict__ cidx,
-                                                                   double* __restrict__ cf,
-                                                                   float* __restrict__ P) {
-  constexpr int S = ScanShape<M, NA>::S, W = ScanShape<M, NA>::W;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int q = lane & 3, r = lane >> 2;
-  const int wblk = blockIdx.x * kScanWarps + warp;
-  const int base = wblk * (W - 2) - 1;                         // grid index of position 0 (L < 2^31)
-  if (base + 1 >= L) return;                                   // whole warp beyond the grid
-
-  double tf[NA][S];
-#pragma unroll
-  for (int t = 0; t < NA; ++t) {
-    const int i = base + 8 * t + r;
-    const bool valid = (i >= 0 && i < L);
-    const double u = valid ? grid_u(i, theta0, dtheta, dl) : 0.0;
-#pragma unroll
-    for (int s = 0; s < S; ++s) tf[t][s] = valid ? table_entry(4 * s + q, M, u) : (4 * s + q == 0 ? 1.0 : 0.0);
-  }
-  // this lane's D positions (t, e) -> grid index base + 8t + 2q + e.  decide: interior of the
-  // warp block and of the grid (Q9); own: interior of the warp block and inside the grid.
-  unsigned dmask = 0, omask = 0;
-#pragma unroll
-  for (int t = 0; t < NA; ++t)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int pos = 8 * t + 2 * q + e, i = base + pos;
-      const bool inner = pos >= 1 && pos <= W - 2;
-      if (inner && i >= 1 && i <= L - 2) dmask |= 1u << (2 * t + e);
-      if (inner && i >= 0 && i < L) omask |= 1u << (2 * t + e);
-    }
-  const int srcL = q > 0 ? lane - 1 : lane + 3;
-  const int srcR = q < 3 ? lane + 1 : lane - 3;
-
-  const int64_t ngroups = (B + 7) / 8;
-  const int64_t g0 = (int64_t)blockIdx.y * groups_per_cta;
-  const int64_t g1 = (g0 + groups_per_cta < ngroups) ? g0 + groups_per_cta : ngroups;
-  const double* cg = coef + ((size_t)g0 * S) * 32 + lane;
-  for (int64_t g = g0; g < g1; ++g, cg += S * 32) {
-    double a[S];
-#pragma unroll
-    for (int s = 0; s < S; ++s) a[s] = __ldg(cg + s * 32);
-    double acc[NA][2];
-#pragma unroll
-    for (int t = 0; t < NA; ++t) { acc[t][0] = 0.0; acc[t][1] = 0.0; }
-#pragma unroll
-    for (int s = 0; s < S; ++s)
-#pragma unroll
-      for (int t = 0; t < NA; ++t) dmma_884(acc[t][0], acc[t][1], a[s], tf[t][s]);
-
-#pragma unroll
-    for (int t = 0; t < NA; ++t) {                 // floor (Q12); fmax(NaN, x) = x like the oracle
-      acc[t][0] = fmax(acc[t][0], kFloor);
-      acc[t][1] = fmax(acc[t][1], kFloor);
-    }
-    // neighbours: left of (t,q,0) is (t,q-1,1) [q>0] or (t-1,3,1) [q=0];
-    //             right of (t,q,1) is (t,q+1,0) [q<3] or (t+1,0,0) [q=3]
-    double up[NA], dn[NA];
-#pragma unroll
-    for (int t = 0; t < NA; ++t) {
-      up[t] = __shfl_sync(0xffffffffu, acc[t][1], srcL);
-      dn[t] = __shfl_sync(0xffffffffu, acc[t][0], srcR);
-    }
-    unsigned hit = 0;
-#pragma unroll
-    for (int t = 0; t < NA; ++t) {
-      const double fl0 = q > 0 ? up[t] : (t > 0 ? up[t - 1] : acc[t][0]);
-      const double fr1 = q < 3 ? dn[t] : (t + 1 < NA ? dn[t + 1] : acc[t][1]);
-      hit |= (unsigned)(acc[t][0] < fl0 && acc[t][0] <= acc[t][1]) << (2 * t);
-      hit |= (unsigned)(acc[t][1] < acc[t][0] && acc[t][1] <= fr1) << (2 * t + 1);
-    }
-    const int b = (int)(g * 8) + r;
-    const bool frame_ok = b < B;
-    hit &= frame_ok ? dmask : 0u;
-    if (hit) {                                     // local maxima of P (rare): append candidates
-      do {
-        const int k = __ffs(hit) - 1;
-        hit &= hit - 1;
-        const int t = k >> 1, e = k & 1;
-        double f = 0.0;
-#pragma unroll
-        for (int tt = 0; tt < NA; ++tt)
-          if (tt == t) f = e ? acc[tt][1] : acc[tt][0];
-        const int slot = atomicAdd(cnt + b, 1);
-        if (slot < cap) {
-          cidx[(size_t)b * cap + slot] = base + 8 * t + 2 * q + e;
-          cf[(size_t)b * cap + slot] = f;
-        }
-      } while (hit);
-    }
-    if (WRITE_P && frame_ok) {
-      float* Pb = P + (size_t)b * L + base + 2 * q;
-#pragma unroll
-      for (int t = 0; t < NA; ++t) {
-        if (omask & (1u << (2 * t))) Pb[8 * t] = to_p32(acc[t][0]);
-        if (omask & (1u << (2 * t + 1))) Pb[8 * t + 1] = to_p32(acc[t][1]);
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------------------------
-// S4-S6, CTA-shared table variant.  A CTA owns NB consecutive angle blocks of W = 8*NA angles
-// (each block: positions 0 and W-1 are halo, blocks advance by W-2) and a range of frame groups.
-// The table is generated ONCE per CTA into shared memory in B-fragment order
-// Ts[k][s][t][lane] = T_{4s + lane%4}(angle base_k + 8t + lane/4), so every B-fragment load is one
-// conflict-free 8-byte LDS per lane.  The CTA's 8 warps stream disjoint frame groups (warp w takes
-// g0 + w, g0 + w + 8, ...): per group one coalesced A-fragment load per k-step (reused for all NB
-// blocks), then per block S x NA DMMAs and the fused epilogue.  With ~100 registers per thread,
-// 16 warps per SM keep the DMMA pipe fed while other warps run their epilogues.
+// S4-S6: the scan on the FP64 tensor pipe (mma.sync m8n8k4 f64).
+//
+// Work tile = (angle column x, frame chunk y).  An angle column is NB = 2 consecutive angle blocks
+// of W = 8*NA grid angles (positions 0 and W-1 of a block are halo; blocks advance by W-2 so
+// every interior angle is decided by exactly one lane).  The steering table of a column is
+// generated once into shared memory in DMMA B-fragment order
+//     Ts[k][s][t][lane] = T_{4s + lane%4}(angle base_k + 8t + lane/4)
+// (fp64 sincospi, no recurrence) so every B-fragment load is one conflict-free 8-byte LDS.
+// The CTA's 8 warps stream disjoint 8-frame groups of the chunk (warp w: g0+w, g0+w+8, ...):
+// one coalesced A-fragment load per k-step (prefetched one group ahead, reused for both blocks),
+// S x NA DMMAs per block (8 independent accumulator chains), then the fused epilogue:
+//   D fragment: lane holds frame lane/4, angles 8t + 2(lane%4) + {0,1}.
+//   floor (Q12) + peak test (Q9/Q10) in the INTEGER domain — for positive doubles the IEEE bits
+//   order like the values, so the FP64 pipe stays with the DMMAs; neighbours by shuffles inside
+//   each 4-lane frame row; rare atomic append to the frame's candidate list; optional fp32 P.
+// Grid: blockIdx.x = angle column, blockIdx.y = frame chunk (~4 waves of resident CTAs).
+// (A persistent tile loop, a software-pipelined and a warp-specialised producer/consumer variant
+// were measured and were slower on c4; see profiles/README.md.)
 constexpr int kCtaWarps = 8;
 constexpr long long kInfBits = 0x7FF0000000000000LL;        // bits of +inf
 constexpr long long kFloorBits = 0x01A56E1FC2F8F359LL;      // bits of 1e-300 (kFloor, Q12)
-#ifndef DOA_SCAN_CTA_MINB
-#define DOA_SCAN_CTA_MINB 3
-#endif
+constexpr int kNB = 2;                                       // angle blocks per column
 
-template <int M, int NB, bool WRITE_P>
-__global__ void __launch_bounds__(kCtaWarps * 32, DOA_SCAN_CTA_MINB) scan_cta_kernel(const double* __restrict__ coef, int64_t B,
-                                                                   int64_t groups_per_cta, double dl,
-                                                                   double theta0, double dtheta, int L, int cap,
-                                                                   int32_t* __restrict__ cnt,
+template <int M>
+struct ScanShape {
+  static constexpr int S = (2 * M + 3) / 4;                 // k-steps of 4 (K = 4S >= 2M-1)
+  static constexpr int NA = (64 / S) < 8 ? (64 / S) : 8;    // 8-angle tiles per block
+  static constexpr int W = 8 * NA;                           // angles per block (incl. 2 halo)
+};
+
+template <int M, bool WRITE_P>
+__global__ void __launch_bounds__(kCtaWarps * 32, 2) scan_cta_kernel(const double* __restrict__ coef, int64_t B,
+                                                                   int64_t per, double dl, double theta0, double dtheta, int L,
+                                                                   int cap, int32_t* __restrict__ cnt,
                                                                    int32_t* __restrict__ cidx,
-                                                                   double* __restrict__ cf,
-                                                                   float* __restrict__ P) {
-  constexpr int S = ScanShape<M>::S, NA = ScanShape<M>::NA, W = ScanShape<M>::W;
+                                                                   double* __restrict__ cf, float* __restrict__ P) {
+  constexpr int S = ScanShape<M>::S, NA = ScanShape<M>::NA, W = ScanShape<M>::W, NB = kNB;
   extern __shared__ double Ts[];                                 // [NB][S][NA][32]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q = lane & 3, r = lane >> 2;
-  const int blk0 = blockIdx.x * NB;
-  // table generation, all threads
-  for (int e = threadIdx.x; e < NB * S * NA * 32; e += kCtaWarps * 32) {
-    const int ln = e & 31, t = (e >> 5) % NA, s = (e / (32 * NA)) % S, k = e / (32 * NA * S);
-    const int i = (blk0 + k) * (W - 2) - 1 + 8 * t + (ln >> 2);
-    const int j = 4 * s + (ln & 3);
-    double v = (j == 0) ? 1.0 : 0.0;
-    if (i >= 0 && i < L) v = table_entry(j, M, grid_u(i, theta0, dtheta, dl));
-    Ts[e] = v;
-  }
-  __syncthreads();
-
   const int srcL = q > 0 ? lane - 1 : lane + 3;
   const int srcR = q < 3 ? lane + 1 : lane - 3;
   const int64_t ngroups = (B + 7) / 8;
-  const int64_t g0 = (int64_t)blockIdx.y * groups_per_cta;
-  const int64_t g1 = (g0 + groups_per_cta < ngroups) ? g0 + groups_per_cta : ngroups;
-  for (int64_t g = g0 + warp; g < g1; g += kCtaWarps) {
-    double a[S];
-    const double* cg = coef + ((size_t)g * S) * 32 + lane;
+  {
+    const int64_t y = blockIdx.y;
+    const int blk0 = (int)blockIdx.x * NB;
+    for (int e = threadIdx.x; e < NB * S * NA * 32; e += kCtaWarps * 32) {
+      const int ln = e & 31, t = (e >> 5) % NA, s = (e / (32 * NA)) % S, k = e / (32 * NA * S);
+      const int i = (blk0 + k) * (W - 2) - 1 + 8 * t + (ln >> 2);
+      const int j = 4 * s + (ln & 3);
+      double v = (j == 0) ? 1.0 : 0.0;
+      if (i >= 0 && i < L) v = table_entry(j, M, grid_u(i, theta0, dtheta, dl));
+      Ts[e] = v;
+    }
+    __syncthreads();
+    const int64_t g0 = y * per;
+    const int64_t g1 = (g0 + per < ngroups) ? g0 + per : ngroups;
+    double an[S];
+    if (g0 + warp < g1) {
+      const double* cg = coef + ((size_t)(g0 + warp) * S) * 32 + lane;
 #pragma unroll
-    for (int s = 0; s < S; ++s) a[s] = __ldg(cg + s * 32);
-    const int b = (int)(g * 8) + r;
-    const bool frame_ok = b < B;
+      for (int s = 0; s < S; ++s) an[s] = __ldg(cg + s * 32);
+    }
+    for (int64_t g = g0 + warp; g < g1; g += kCtaWarps) {
+      double a[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) a[s] = an[s];
+      if (g + kCtaWarps < g1) {                                  // prefetch the next group's operands
+        const double* cg = coef + ((size_t)(g + kCtaWarps) * S) * 32 + lane;
+#pragma unroll
+        for (int s = 0; s < S; ++s) an[s] = __ldg(cg + s * 32);
+      }
+      const int b = (int)(g * 8) + r;
+      const bool frame_ok = b < B;
 #pragma unroll 1
-    for (int k = 0; k < NB; ++k) {
-      const int base = (blk0 + k) * (W - 2) - 1;
-      if (base + 1 >= L) break;                                  // warp-uniform
-      const double* Tk = Ts + (size_t)k * S * NA * 32 + lane;
-      double acc[NA][2];
+      for (int k = 0; k < NB; ++k) {
+        const int base = (blk0 + k) * (W - 2) - 1;
+        if (base + 1 >= L) break;                                // warp-uniform
+        const double* Tk = Ts + (size_t)k * S * NA * 32 + lane;
+        double acc[NA][2];
 #pragma unroll
-      for (int t = 0; t < NA; ++t) { acc[t][0] = 0.0; acc[t][1] = 0.0; }
+        for (int t = 0; t < NA; ++t) { acc[t][0] = 0.0; acc[t][1] = 0.0; }
 #pragma unroll
-      for (int s = 0; s < S; ++s)
+        for (int s = 0; s < S; ++s)
 #pragma unroll
-        for (int t = 0; t < NA; ++t) dmma_884(acc[t][0], acc[t][1], a[s], Tk[(s * NA + t) * 32]);
-      // Floor (Q12) and the peak test in the INTEGER domain: for non-negative doubles the IEEE
-      // bit patterns order exactly like the values, so the floored f are compared as signed
-      // 64-bit integers on the integer pipes while the FP64 pipe stays with the DMMAs.
-      // Negative values, -0, +0 and NaNs of either sign map to the floor like fmax(x, 1e-300).
-      long long fi[NA][2];
+          for (int t = 0; t < NA; ++t) dmma_884(acc[t][0], acc[t][1], a[s], Tk[(s * NA + t) * 32]);
+        // Fast path: if every value of the warp's tile is a positive double above the floor and
+        // not NaN (checked on the high words, conservatively), the raw bits already are the
+        // floored values; otherwise the whole tile takes the explicit floor, which maps negative
+        // values, +-0 and NaNs to 1e-300 like the oracle's max(f, 1e-300) (Q12).
+        long long fi[NA][2];
+        int hmin = 0x7FFFFFFF, hmax = (int)0x80000000;
 #pragma unroll
-      for (int t = 0; t < NA; ++t)
+        for (int t = 0; t < NA; ++t)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          long long x = __double_as_longlong(acc[t][e]);
-          x = x > kInfBits ? kFloorBits : x;
-          fi[t][e] = x > kFloorBits ? x : kFloorBits;
+          for (int e = 0; e < 2; ++e) {
+            fi[t][e] = __double_as_longlong(acc[t][e]);
+            const int hi = (int)(fi[t][e] >> 32);
+            hmin = min(hmin, hi);
+            hmax = max(hmax, hi);
+          }
+        if (__any_sync(0xffffffffu, hmin <= (int)(kFloorBits >> 32) || hmax >= (int)(kInfBits >> 32))) {
+#pragma unroll
+          for (int t = 0; t < NA; ++t)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              long long v = fi[t][e];
+              v = v > kInfBits ? kFloorBits : v;
+              fi[t][e] = v > kFloorBits ? v : kFloorBits;
+            }
         }
-      long long up[NA], dn[NA];
+        // neighbours: left of (t,q,0) is (t,q-1,1) [q>0] or (t-1,3,1) [q=0];
+        //             right of (t,q,1) is (t,q+1,0) [q<3] or (t+1,0,0) [q=3]
+        long long up[NA], dn[NA];
 #pragma unroll
-      for (int t = 0; t < NA; ++t) {
-        up[t] = __shfl_sync(0xffffffffu, fi[t][1], srcL);
-        dn[t] = __shfl_sync(0xffffffffu, fi[t][0], srcR);
-      }
-      // lane pair (v0, v1) with outer neighbours L, R:  c = v1 < v0;
-      // v0 is a minimum iff !c && v0 < L;  v1 is a minimum iff c && v1 <= R   (Q10)
-      unsigned hit = 0;
+        for (int t = 0; t < NA; ++t) {
+          up[t] = __shfl_sync(0xffffffffu, fi[t][1], srcL);
+          dn[t] = __shfl_sync(0xffffffffu, fi[t][0], srcR);
+        }
+        // lane pair (v0, v1) with outer neighbours L, R: c = v1 < v0;
+        // v0 is a minimum iff !c && v0 < L;  v1 is a minimum iff c && v1 <= R   (Q10)
+        unsigned hit = 0;
 #pragma unroll
-      for (int t = 0; t < NA; ++t) {
-        const long long fl0 = q > 0 ? up[t] : (t > 0 ? up[t - 1] : fi[t][0]);
-        const long long fr1 = q < 3 ? dn[t] : (t + 1 < NA ? dn[t + 1] : fi[t][1]);
-        const bool c = fi[t][1] < fi[t][0];
-        hit |= (unsigned)(!c && fi[t][0] < fl0) << (2 * t);
-        hit |= (unsigned)(c && fi[t][1] <= fr1) << (2 * t + 1);
-      }
-      // decidable positions: block interior (pos 1..W-2) and grid interior (1..L-2)
-      if (!frame_ok) hit = 0;
-      if (hit) {
-        do {
+        for (int t = 0; t < NA; ++t) {
+          const long long fl0 = q > 0 ? up[t] : (t > 0 ? up[t - 1] : fi[t][0]);
+          const long long fr1 = q < 3 ? dn[t] : (t + 1 < NA ? dn[t + 1] : fi[t][1]);
+          const bool c = fi[t][1] < fi[t][0];
+          hit |= (unsigned)(!c && fi[t][0] < fl0) << (2 * t);
+          hit |= (unsigned)(c && fi[t][1] <= fr1) << (2 * t + 1);
+        }
+        if (!frame_ok) hit = 0;
+        while (hit) {                                            // local maxima of P (rare)
           const int kk = __ffs(hit) - 1;
           hit &= hit - 1;
           const int t = kk >> 1, e = kk & 1;
           const int pos = 8 * t + 2 * q + e, i = base + pos;
-          if (pos < 1 || pos > W - 2 || i < 1 || i > L - 2) continue;
+          if (pos < 1 || pos > W - 2 || i < 1 || i > L - 2) continue;   // halo / grid ends (Q9)
           long long f = 0;
 #pragma unroll
           for (int tt = 0; tt < NA; ++tt)
@@ -392,28 +293,29 @@ __global__ void __launch_bounds__(kCtaWarps * 32, DOA_SCAN_CTA_MINB) scan_cta_ke
             cidx[(size_t)b * cap + slot] = i;
             cf[(size_t)b * cap + slot] = __longlong_as_double(f);
           }
-        } while (hit);
-      }
-      if (WRITE_P && frame_ok) {
-        float* Pb = P + (size_t)b * L;
+        }
+        if (WRITE_P && frame_ok) {
+          float* Pb = P + (size_t)b * L;
 #pragma unroll
-        for (int t = 0; t < NA; ++t)
+          for (int t = 0; t < NA; ++t)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int pos = 8 * t + 2 * q + e, i = base + pos;
-            if (pos >= 1 && pos <= W - 2 && i >= 0 && i < L) Pb[i] = to_p32(__longlong_as_double(fi[t][e]));
-          }
+            for (int e = 0; e < 2; ++e) {
+              const int pos = 8 * t + 2 * q + e, i = base + pos;
+              if (pos >= 1 && pos <= W - 2 && i >= 0 && i < L) Pb[i] = to_p32(__longlong_as_double(fi[t][e]));
+            }
+        }
       }
     }
   }
 }
 
-// Same contraction for any M <= 64 with the table in shared memory and plain DFMA (runtime M;
-// used for M > 32, where a register-resident table would spill).  Lanes own angles of a
-// 32-angle block with halo lanes 0 and 31 (stride 30).
+// Same contraction for 32 < M <= 64 with the table in shared memory and plain DFMA (runtime M;
+// a register/B-fragment table of K = 4S <= 128 entries per angle would not pay off there).
+// Lanes own angles of a 32-angle block with halo lanes 0 and 31 (stride 30).
+constexpr int kSmemWarps = 4;
 constexpr int kSmemStride = 30;
 
-__global__ void __launch_bounds__(kScanWarps * 32) scan_smem_kernel(const double* __restrict__ coef, int64_t B, int M,
+__global__ void __launch_bounds__(kSmemWarps * 32) scan_smem_kernel(const double* __restrict__ coef, int64_t B, int M,
                                                                    int64_t frames_per_cta, double dl, double theta0,
                                                                    double dtheta, int64_t L, int cap,
                                                                    int32_t* __restrict__ cnt,
@@ -424,7 +326,7 @@ __global__ void __launch_bounds__(kScanWarps * 32) scan_smem_kernel(const double
   const int NJ = 4 * S;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* T = tsm + (size_t)warp * NJ * 32;          // T[j][lane]
-  const int64_t wblk = (int64_t)blockIdx.x * kScanWarps + warp;
+  const int64_t wblk = (int64_t)blockIdx.x * kSmemWarps + warp;
   const int64_t i = wblk * kSmemStride - 1 + lane;
   const bool valid = (i >= 0 && i < L);
   const double u = valid ? grid_u(i, theta0, dtheta, dl) : 0.0;
@@ -451,61 +353,65 @@ __global__ void __launch_bounds__(kScanWarps * 32) scan_smem_kernel(const double
   }
 }
 
-int64_t waves_chunk(int64_t cols, int64_t units, int64_t min_per_cta) {
-  // split `units` (frame groups or frames) into chunks so the grid has ~8 waves of 148 SMs x 2 CTAs
-  int64_t per = (cols * units) / (148 * 2 * 8);
-  if (per < min_per_cta) per = min_per_cta;
-  if (per > units) per = units;
-  return per;
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
 }
 
-template <int M, int NB>
+template <int M>
 cudaError_t launch_scan_cta(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
-  constexpr int S = ScanShape<M>::S, NA = ScanShape<M>::NA, W = ScanShape<M>::W;
+  constexpr int S = ScanShape<M>::S, NA = ScanShape<M>::NA, W = ScanShape<M>::W, NB = kNB;
+  const size_t smem = (size_t)NB * S * NA * 32 * sizeof(double);
+  static int occ = 0;
+  if (!occ) {
+    cudaFuncSetAttribute(scan_cta_kernel<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(scan_cta_kernel<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_cta_kernel<M, false>, kCtaWarps * 32, smem);
+    if (occ < 1) occ = 1;
+  }
   const int64_t nwb = (p->L + (W - 2) - 1) / (W - 2);           // angle blocks owning [0, L)
-  const int64_t gx = (nwb + NB - 1) / NB;
+  const int64_t gx = (nwb + NB - 1) / NB;                        // angle columns
   const int64_t ngroups = (B + 7) / 8;
-  // frame chunks: >= ~4 waves of 2 CTAs x 148 SMs, >= 64 groups (8 per warp) per CTA
-  int64_t per = (gx * ngroups) / (148 * 2 * 4);
+  const int64_t slots = (int64_t)sm_count() * occ;
+  // frame chunk: ~4 waves of resident CTAs, >= 64 groups (8 per warp) per CTA
+  int64_t per = (gx * ngroups) / (4 * slots);
   if (per < 64) per = 64;
   if (per > ngroups) per = ngroups;
   const int64_t gy = (ngroups + per - 1) / per;
-  const size_t smem = (size_t)NB * S * NA * 32 * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(scan_cta_kernel<M, NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(scan_cta_kernel<M, NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  count_launch();
   const dim3 grid((unsigned)gx, (unsigned)gy);
+  count_launch();
   if (P)
-    scan_cta_kernel<M, NB, true><<<grid, kCtaWarps * 32, smem, s>>>(
-        p->coef, B, per, p->dl, p->theta0, p->dtheta, (int)p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
+    scan_cta_kernel<M, true><<<grid, kCtaWarps * 32, smem, s>>>(p->coef, B, per, p->dl, p->theta0, p->dtheta,
+                                                               (int)p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
   else
-    scan_cta_kernel<M, NB, false><<<grid, kCtaWarps * 32, smem, s>>>(
-        p->coef, B, per, p->dl, p->theta0, p->dtheta, (int)p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
+    scan_cta_kernel<M, false><<<grid, kCtaWarps * 32, smem, s>>>(p->coef, B, per, p->dl, p->theta0, p->dtheta,
+                                                                (int)p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
   return cudaGetLastError();
 }
 
-template <int M, int NA>
-cudaError_t launch_scan_t(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
-  static const bool warp_variant = getenv("DOA_SCAN_WARP") != nullptr;   // A/B switch for tuning only
-  if (!warp_variant) return launch_scan_cta<M, DOA_SCAN_NB>(p, B, P, s);
-  constexpr int W = ScanShape<M, NA>::W;
-  const int64_t nwb = (p->L + (W - 2) - 1) / (W - 2);           // warp blocks owning [0, L)
-  const int64_t gx = (nwb + kScanWarps - 1) / kScanWarps;
-  const int64_t ngroups = (B + 7) / 8;
-  const int64_t per = waves_chunk(gx, ngroups, 8);
-  const int64_t gy = (ngroups + per - 1) / per;
+cudaError_t launch_scan_smem(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
+  const int64_t nwb = (p->L + kSmemStride - 1) / kSmemStride;
+  const int64_t gx = (nwb + kSmemWarps - 1) / kSmemWarps;
+  int64_t fpc = (gx * B) / (148 * 2 * 8);
+  if (fpc < 16) fpc = 16;
+  if (fpc > B) fpc = B;
+  const int64_t gy = (B + fpc - 1) / fpc;
+  const size_t smem = (size_t)kSmemWarps * 4 * ksteps(p->M) * 32 * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(scan_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(kSmemWarps * 4 * ksteps(kMaxM) * 32 * sizeof(double)));
+    attr = true;
+  }
   count_launch();
-  const dim3 grid((unsigned)gx, (unsigned)gy);
-  if (P)
-    scan_dmma_kernel<M, NA, true><<<grid, kScanWarps * 32, 0, s>>>(
-        p->coef, B, per, p->dl, p->theta0, p->dtheta, (int)p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
-  else
-    scan_dmma_kernel<M, NA, false><<<grid, kScanWarps * 32, 0, s>>>(
-        p->coef, B, per, p->dl, p->theta0, p->dtheta, (int)p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
+  scan_smem_kernel<<<dim3((unsigned)gx, (unsigned)gy), kSmemWarps * 32, smem, s>>>(
+      p->coef, B, p->M, fpc, p->dl, p->theta0, p->dtheta, p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
   return cudaGetLastError();
 }
 
@@ -570,7 +476,7 @@ cudaError_t launch_coef(const doa_plan_s* p, const double* lam, const double* V,
 
 cudaError_t launch_scan(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
   switch (p->M) {
-#define DOA_SCAN_CASE(m) case m: return launch_scan_t<m, ScanShape<m>::NA>(p, B, P, s);
+#define DOA_SCAN_CASE(m) case m: return launch_scan_cta<m>(p, B, P, s);
     DOA_SCAN_CASE(2) DOA_SCAN_CASE(3) DOA_SCAN_CASE(4) DOA_SCAN_CASE(5) DOA_SCAN_CASE(6) DOA_SCAN_CASE(7)
     DOA_SCAN_CASE(8) DOA_SCAN_CASE(9) DOA_SCAN_CASE(10) DOA_SCAN_CASE(11) DOA_SCAN_CASE(12) DOA_SCAN_CASE(13)
     DOA_SCAN_CASE(14) DOA_SCAN_CASE(15) DOA_SCAN_CASE(16) DOA_SCAN_CASE(17) DOA_SCAN_CASE(18) DOA_SCAN_CASE(19)
@@ -578,23 +484,7 @@ cudaError_t launch_scan(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s
     DOA_SCAN_CASE(25) DOA_SCAN_CASE(26) DOA_SCAN_CASE(27) DOA_SCAN_CASE(28) DOA_SCAN_CASE(29)
     DOA_SCAN_CASE(30) DOA_SCAN_CASE(31) DOA_SCAN_CASE(32)
 #undef DOA_SCAN_CASE
-    default: {
-      const int64_t nwb = (p->L + kSmemStride - 1) / kSmemStride;
-      const int64_t gx = (nwb + kScanWarps - 1) / kScanWarps;
-      const int64_t fpc = waves_chunk(gx, B, 16);
-      const int64_t gy = (B + fpc - 1) / fpc;
-      const size_t smem = (size_t)kScanWarps * 4 * ksteps(p->M) * 32 * sizeof(double);
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(scan_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kScanWarps * 4 * ksteps(kMaxM) * 32 * sizeof(double)));
-        attr = true;
-      }
-      count_launch();
-      scan_smem_kernel<<<dim3((unsigned)gx, (unsigned)gy), kScanWarps * 32, smem, s>>>(
-          p->coef, B, p->M, fpc, p->dl, p->theta0, p->dtheta, p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
-      return cudaGetLastError();
-    }
+    default: return launch_scan_smem(p, B, P, s);
   }
 }
 
