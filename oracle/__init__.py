@@ -56,6 +56,15 @@ def lib():
                                            C.c_int64, fp, C.c_int64, C.c_int64, i32p, fp, i32p, i32p, i32p,
                                            fp, C.c_int]
             L.oracle_run_batch.restype = None
+            L.oracle_spectrum_array.argtypes = [C.c_int, C.c_int, C.c_int, dp, dp, dp, C.c_double, C.c_double,
+                                                C.c_int64, C.c_double, C.c_double, C.c_int64, dp, C.c_int, ip]
+            L.oracle_spectrum_array.restype = None
+            L.oracle_peaks2d.argtypes = [dp, C.c_int64, C.c_int64, C.c_int, C.c_int, i32p, dp, i32p]
+            L.oracle_peaks2d.restype = C.c_int64
+            L.oracle_run_array_batch.argtypes = [C.c_int, C.c_int, C.c_int, dp, C.c_double, C.c_double, C.c_int64,
+                                                 C.c_double, C.c_double, C.c_int64, C.c_int, fp, C.c_int64,
+                                                 C.c_int64, i32p, fp, i32p, i32p, fp, C.c_int]
+            L.oracle_run_array_batch.restype = None
             _lib = L
     return _lib
 
@@ -139,3 +148,49 @@ def run_batch(alg: str, X: np.ndarray, D: int, d_over_lambda: float, theta0: flo
                            B, N, _p(idx, C.c_int32), _p(val, C.c_float), _p(npk, C.c_int32), _p(info, C.c_int32),
                            _p(sweeps, C.c_int32), _p(P, C.c_float) if want_P else None, threads)
     return dict(idx=idx, val=val, npk=npk, info=info, sweeps=sweeps, P=P)
+
+
+# ---------------------------------------------------------------------------- NEXT-1: general arrays
+def spectrum_array(alg: str, D: int, pos, lam, V, az0, daz, naz, el0, del_, nel, threads: int = 1):
+    """Eq. 2 steering for element positions pos[M][3] (wavelengths) over the azimuth-major
+    az x el grid -> (f[naz*nel], info)."""
+    V = _c128(V)
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+    M = V.shape[0]
+    f = np.empty(naz * nel)
+    info = C.c_int(0)
+    lib().oracle_spectrum_array(ALG[alg], M, D, _p(pos, C.c_double), _p(lam, C.c_double),
+                                _p(V.view(np.float64), C.c_double), az0, daz, naz, el0, del_, nel,
+                                _p(f, C.c_double), threads, C.byref(info))
+    return f, info.value
+
+
+def peaks2d(f, naz: int, nel: int, wrap: bool, D: int):
+    """2-D findPeaks (8-neighbourhood, raster tie rule, optional azimuth wrap) + PeakSelection
+    -> (idx[D] raster indices (-1 pad), fval[D], npk, n_candidates)."""
+    f = np.ascontiguousarray(f, dtype=np.float64).reshape(-1)
+    idx = np.empty(D, dtype=np.int32)
+    fv = np.empty(D)
+    npk = C.c_int32(0)
+    n = lib().oracle_peaks2d(_p(f, C.c_double), naz, nel, int(bool(wrap)), D, _p(idx, C.c_int32),
+                             _p(fv, C.c_double), C.byref(npk))
+    return idx, fv, npk.value, n
+
+
+def run_array_batch(alg: str, X, D: int, pos, az0, daz, naz, el0, del_, nel, wrap: bool, threads: int = 1,
+                    want_P: bool = False):
+    X = np.ascontiguousarray(X, dtype=np.complex64)
+    B, N, M = X.shape
+    pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+    L = naz * nel
+    idx = np.empty((B, D), dtype=np.int32)
+    val = np.empty((B, D), dtype=np.float32)
+    npk = np.empty(B, dtype=np.int32)
+    info = np.empty(B, dtype=np.int32)
+    P = np.empty((B, L), dtype=np.float32) if want_P else None
+    lib().oracle_run_array_batch(ALG[alg], M, D, _p(pos, C.c_double), az0, daz, naz, el0, del_, nel,
+                                 int(bool(wrap)), _p(X.view(np.float32), C.c_float), B, N, _p(idx, C.c_int32),
+                                 _p(val, C.c_float), _p(npk, C.c_int32), _p(info, C.c_int32),
+                                 _p(P, C.c_float) if want_P else None, threads)
+    return dict(idx=idx, val=val, npk=npk, info=info, P=P)

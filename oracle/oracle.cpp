@@ -224,6 +224,72 @@ int64_t peaks(const double* f, int64_t L, int D, int32_t* idx, double* fval, int
   return (int64_t)cand.size();
 }
 
+// general array geometry on an azimuth x elevation grid (the paper's own
+// UCA workload).  Steering is Eq. 2 written out per element, with
+// positions in wavelengths: a_k = exp{ j 2 pi (x_k sin(az) sin(el) + y_k cos(az) sin(el) +
+// z_k cos(el)) }; grid az_i = az0 + i*daz, el_j = el0 + j*del (multiply then add), flattened
+// azimuth-major p = i*nel + j.  invP = sum_k w_k |u_k^H a|^2, floored (Q12).
+void spectrum_array(const Subspace& S, int M, const double* pos, double az0, double daz, int64_t nel,
+                    double el0, double del, int64_t p0, int64_t p1, double* f) {
+  const double pi = 3.14159265358979323846;
+  std::vector<cd> a(M);
+  for (int64_t p = p0; p < p1; ++p) {
+    const int64_t ia = p / nel, ie = p % nel;
+    const double az = (az0 + (double)ia * daz) * pi / 180.0;
+    const double el = (el0 + (double)ie * del) * pi / 180.0;
+    for (int m = 0; m < M; ++m) {
+      const double ph = 2.0 * pi * (pos[3 * m] * std::sin(az) * std::sin(el) +
+                                    pos[3 * m + 1] * std::cos(az) * std::sin(el) + pos[3 * m + 2] * std::cos(el));
+      a[m] = cd(std::cos(ph), std::sin(ph));
+    }
+    double acc = 0.0;
+    for (size_t k = 0; k < S.u.size(); ++k) {
+      cd ip(0.0, 0.0);
+      for (int m = 0; m < M; ++m) ip += std::conj(S.u[k][m]) * a[m];
+      acc += S.w[k] * std::norm(ip);
+    }
+    f[p] = acc > F_FLOOR ? acc : F_FLOOR;
+  }
+}
+
+// 2-D findPeaks (reading DESIGN.md G2): p is a local minimum of f (maximum of P) iff for each of
+// its 8 neighbours n: f_p < f_n when n precedes p in raster order, f_p <= f_n when it follows
+// (a plateau collapses to its first raster point).  Azimuth wraps when `wrap`; neighbours beyond
+// the elevation range (or the azimuth range without wrap) do not exist.  Then PeakSelection as
+// in 1-D: order by (f ascending, raster index ascending), keep min(D, count).
+int64_t peaks2d(const double* f, int64_t naz, int64_t nel, int wrap, int D, int32_t* idx, double* fval,
+                int32_t* npk) {
+  std::vector<std::pair<double, int64_t>> cand;
+  for (int64_t ia = 0; ia < naz; ++ia)
+    for (int64_t ie = 0; ie < nel; ++ie) {
+      const int64_t p = ia * nel + ie;
+      bool peak = true;
+      for (int da = -1; da <= 1 && peak; ++da)
+        for (int de = -1; de <= 1 && peak; ++de) {
+          if (da == 0 && de == 0) continue;
+          int64_t ja = ia + da;
+          const int64_t je = ie + de;
+          if (je < 0 || je >= nel) continue;
+          if (ja < 0 || ja >= naz) {
+            if (!wrap) continue;
+            ja = (ja + naz) % naz;
+          }
+          const int64_t n = ja * nel + je;
+          if (n == p) continue;
+          if (n < p ? !(f[p] < f[n]) : !(f[p] <= f[n])) peak = false;
+        }
+      if (peak) cand.push_back({f[p], p});
+    }
+  std::sort(cand.begin(), cand.end());
+  const int n = (int)std::min<int64_t>(D, (int64_t)cand.size());
+  for (int k = 0; k < D; ++k) {
+    idx[k] = k < n ? (int32_t)cand[k].second : -1;
+    fval[k] = k < n ? cand[k].first : 0.0;
+  }
+  *npk = n;
+  return (int64_t)cand.size();
+}
+
 // P = 1/f_c reported in fp32, saturating at FLT_MAX.
 float to_p32(double f) {
   const double p = 1.0 / f;
@@ -322,6 +388,67 @@ void oracle_run_batch(int alg, int M, int D, double dl, double theta0, double dt
       if (npk[b] < D) inf |= INFO_UNDERDETERMINED;
       info[b] = inf;
       if (sweeps) sweeps[b] = sw;
+      if (P)
+        for (int64_t i = 0; i < L; ++i) P[(size_t)b * L + i] = to_p32(f[i]);
+    }
+  };
+  if (nthreads <= 1 || B == 1) {
+    work(0, B);
+  } else {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nthreads; ++t) {
+      const int64_t a = B * t / nthreads, c = B * (t + 1) / nthreads;
+      if (a < c) th.emplace_back(work, a, c);
+    }
+    for (auto& x : th) x.join();
+  }
+}
+
+// NEXT-1: spectrum of a general array on the az x el grid (f_c[naz*nel], azimuth-major).
+void oracle_spectrum_array(int alg, int M, int D, const double* pos, const double* lam, const double* V,
+                           double az0, double daz, int64_t naz, double el0, double del, int64_t nel, double* f,
+                           int nthreads, int* info) {
+  std::vector<double> l(lam, lam + M);
+  int inf = 0;
+  Subspace S = noise_subspace(alg, M, D, l, unpack(V, (size_t)M * M), &inf);
+  const int64_t L = naz * nel;
+  if (nthreads <= 1) {
+    spectrum_array(S, M, pos, az0, daz, nel, el0, del, 0, L, f);
+  } else {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nthreads; ++t) {
+      const int64_t a = L * t / nthreads, b = L * (t + 1) / nthreads;
+      th.emplace_back([&, a, b] { spectrum_array(S, M, pos, az0, daz, nel, el0, del, a, b, f); });
+    }
+    for (auto& x : th) x.join();
+  }
+  *info = inf;
+}
+
+int64_t oracle_peaks2d(const double* f, int64_t naz, int64_t nel, int wrap, int D, int32_t* idx, double* fval,
+                       int32_t* npk) {
+  return peaks2d(f, naz, nel, wrap, D, idx, fval, npk);
+}
+
+// NEXT-1 whole path for a batch of frames of a general array.
+void oracle_run_array_batch(int alg, int M, int D, const double* pos, double az0, double daz, int64_t naz,
+                            double el0, double del, int64_t nel, int wrap, const float* X, int64_t B, int64_t N,
+                            int32_t* idx, float* val, int32_t* npk, int32_t* info, float* P, int nthreads) {
+  const int64_t L = naz * nel;
+  auto work = [&](int64_t b0, int64_t b1) {
+    std::vector<double> f((size_t)L), fv(D);
+    std::vector<cd> R, V;
+    std::vector<double> lam;
+    for (int64_t b = b0; b < b1; ++b) {
+      int inf = 0;
+      covariance(X + (size_t)b * N * M * 2, N, M, R);
+      eig(R, M, lam, V, &inf);
+      Subspace S = noise_subspace(alg, M, D, lam, V, &inf);
+      spectrum_array(S, M, pos, az0, daz, nel, el0, del, 0, L, f.data());
+      peaks2d(f.data(), naz, nel, wrap, D, idx + b * D, fv.data(), npk + b);
+      for (int k = 0; k < D; ++k) val[b * D + k] = k < npk[b] ? to_p32(fv[k]) : 0.0f;
+      if (npk[b] < D) inf |= INFO_UNDERDETERMINED;
+      info[b] = inf;
       if (P)
         for (int64_t i = 0; i < L; ++i) P[(size_t)b * L + i] = to_p32(f[i]);
     }
