@@ -79,6 +79,23 @@ doa_status_t doa_plan_create(doa_plan_t* plan, int32_t M, double d_over_lambda, 
                              double theta0_deg, double dtheta_deg, int64_t L, int32_t alg,
                              int64_t max_batch);
 
+/* General array geometry on an azimuth x elevation grid (the paper's own UCA
+ * workload).  positions: HOST double [M][3], element coordinates in
+ * wavelengths; steering is Eq. 2, a_k = exp{ j 2 pi (x_k sin(az) sin(el) + y_k cos(az)
+ * sin(el) + z_k cos(el)) } with el measured from +z (el = 90 deg is the xy plane; the paper's
+ * naming).  Grid az_i = az0 + i*daz (i < naz), el_j = el0 + j*del (j < nel), flattened
+ * azimuth-major p = i*nel + j; L = naz*nel in [3, 2^31).  az_wrap != 0: azimuth neighbours wrap
+ * (a full 360-degree azimuth range).  M in [2, 16] (M > 16: DOA_ERR_UNSUPPORTED); 1 <= D < M.
+ * doa_covariance / doa_eig are as for ULA plans; doa_spectrum computes f on the grid (P, when
+ * given, is float [B][naz][nel]) and the 2-D local maxima of P (8-neighbourhood; a neighbour
+ * earlier in raster order must be strictly larger in f, a later one larger or equal; neighbours
+ * outside the grid are ignored — DESIGN.md G2); doa_peaks returns raster indices p.  Allocates an
+ * fp64 spectrum buffer of max_batch * L doubles. */
+doa_status_t doa_plan_create_array(doa_plan_t* plan, int32_t M, const double* positions, int32_t D,
+                                   double az0_deg, double daz_deg, int64_t naz, double el0_deg,
+                                   double del_deg, int64_t nel, int32_t az_wrap, int32_t alg,
+                                   int64_t max_batch);
+
 /* Free the plan and its workspace (synchronises the device).  NULL is a no-op. */
 doa_status_t doa_plan_destroy(doa_plan_t plan);
 

@@ -18,7 +18,7 @@ INFO_NOCONV, INFO_DEGENERATE, INFO_CAND_OVERFLOW, INFO_UNDERDETERMINED = 1, 2, 4
 STATUS = {0: "DOA_OK", 1: "DOA_ERR_INVALID_ARG", 2: "DOA_ERR_UNSUPPORTED", 3: "DOA_ERR_OUT_OF_MEMORY",
           4: "DOA_ERR_CUDA"}
 
-EXPORTS = ("doa_plan_create", "doa_plan_destroy", "doa_plan_capacity", "doa_covariance", "doa_eig",
+EXPORTS = ("doa_plan_create", "doa_plan_create_array", "doa_plan_destroy", "doa_plan_capacity", "doa_covariance", "doa_eig",
            "doa_spectrum", "doa_peaks", "doa_run", "doa_run_host", "doa_last_launch_count",
            "doa_status_string", "doa_last_error", "doa_version")
 
@@ -35,6 +35,8 @@ def _load():
     L = C.CDLL(LIB_PATH)
     vp, dp, fp, i32p, i64, i32, d = C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_double
     L.doa_plan_create.argtypes = [C.POINTER(C.c_void_p), i32, d, i32, d, d, i64, i32, i64]
+    L.doa_plan_create_array.argtypes = [C.POINTER(C.c_void_p), i32, C.POINTER(C.c_double), i32, d, d, i64, d, d,
+                                        i64, i32, i32, i64]
     L.doa_plan_destroy.argtypes = [vp]
     L.doa_plan_capacity.argtypes = [vp]
     L.doa_plan_capacity.restype = i32
@@ -103,6 +105,17 @@ def doa_plan_create(M, d_over_lambda, D, theta0_deg, dtheta_deg, L, alg, max_bat
     return h
 
 
+def doa_plan_create_array(M, positions, D, az0_deg, daz_deg, naz, el0_deg, del_deg, nel, az_wrap, alg, max_batch):
+    """positions: (M, 3) element coordinates in wavelengths (host array-like)."""
+    import numpy as np
+    pos = np.ascontiguousarray(positions, dtype=np.float64).reshape(M, 3)
+    h = C.c_void_p()
+    a = ALG[alg] if isinstance(alg, str) else int(alg)
+    _check(lib.doa_plan_create_array(C.byref(h), M, pos.ctypes.data_as(C.POINTER(C.c_double)), D, az0_deg, daz_deg,
+                                     naz, el0_deg, del_deg, nel, int(bool(az_wrap)), a, max_batch))
+    return h
+
+
 def doa_plan_destroy(plan):
     _check(lib.doa_plan_destroy(plan))
 
@@ -159,6 +172,21 @@ class Plan:
         self.max_batch = max_batch
         self.h = doa_plan_create(M, d_over_lambda, D, theta0, dtheta, L, alg, max_batch)
         self.cap = int(lib.doa_plan_capacity(self.h))
+
+    @classmethod
+    def array(cls, positions, D, alg, az0=0.0, daz=1.0, naz=360, el0=90.0, del_=1.0, nel=1, az_wrap=True,
+              max_batch=1, device="cuda"):
+        """General-geometry plan on an azimuth x elevation grid (doa_plan_create_array)."""
+        self = cls.__new__(cls)
+        M = len(positions)
+        self.M, self.D, self.alg, self.L = M, D, alg, naz * nel
+        self.naz, self.nel = naz, nel
+        self.device = torch.device(device)
+        self.max_batch = max_batch
+        self.h = None
+        self.h = doa_plan_create_array(M, positions, D, az0, daz, naz, el0, del_, nel, az_wrap, alg, max_batch)
+        self.cap = int(lib.doa_plan_capacity(self.h))
+        return self
 
     def close(self):
         if self.h is not None:

@@ -1,0 +1,283 @@
+// general array geometry on an azimuth x elevation grid — the paper's own
+// workload (8-element UCA; scan ranges 360 x {1, 30, 60, 90}).
+//
+// Steering is Eq. 2 with positions in wavelengths.  Without the ULA's Toeplitz structure
+// the quadratic form still reduces to a real contraction: with z_pq = conj(a_p) a_q =
+// exp(j 2 pi (r_q - r_p) . u(az, el)),
+//     f = a^H C a = sum_p C_pp + 2 sum_{p<q} ( Re C_pq cos(phi_pq) - Im C_pq sin(phi_pq) ),
+// K = 1 + M(M-1) terms per (frame, angle) against a per-angle table shared by all frames, so the
+// scan runs on the same FP64 DMMA machinery as the ULA path (table in shared memory in B-fragment
+// order, coefficients in the A-fragment layout).  The 2-D peak search (8-neighbourhood, azimuth
+// wrap, raster tie rule — DESIGN.md G2) runs on the floored f written to the plan's buffer.
+#include <cfloat>
+
+#include "doa_internal.cuh"
+
+namespace doa {
+namespace {
+
+constexpr double kFloorA = 1e-300;          // Q12
+
+__device__ __forceinline__ float to_p32a(double f) {
+  const double p = 1.0 / f;
+  return p > (double)FLT_MAX ? FLT_MAX : (float)p;
+}
+
+__device__ __forceinline__ void dmma_a(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void pair_of(int idx, int M, int& p, int& q) {
+  p = 0;
+  while (idx >= M - 1 - p) { idx -= M - 1 - p; ++p; }
+  q = p + 1 + idx;
+}
+
+// S3 for general arrays: one warp per frame; same noise-subspace objects as the ULA path
+// (Table 3, Q1/Q5, G1), then c_0 = trace C and (2 Re C_pq, -2 Im C_pq) for p < q,
+// C_pq = sum_j w_j u_j[p] conj(u_j[q]), written in the DMMA A-fragment layout.
+__global__ void __launch_bounds__(128) coef_array_kernel(const double* __restrict__ lam,
+                                                        const double2* __restrict__ V, int64_t B, int M, int D,
+                                                        int alg, double* __restrict__ coef,
+                                                        int32_t* __restrict__ cnt, int32_t* __restrict__ info) {
+  __shared__ double2 Us[4][16 * 17];
+  __shared__ double ws[4][16];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t b = (int64_t)blockIdx.x * 4 + warp;
+  if (b >= B) return;
+  const int ld = 17;
+  double2* U = Us[warp];
+  const int S = array_ksteps(M), K = array_terms(M);
+  const double2* Vb = V + (size_t)b * M * M;
+  const double* lb = lam + (size_t)b * M;
+  const int Kn = M - D;
+  int flag = 0;
+  const int nload = (alg == DOA_ALG_PHD) ? 1 : Kn;
+  for (int e = lane; e < M * M; e += 32) {
+    const int p = e / M, j = e - (e / M) * M;
+    if (j < nload) U[j * ld + p] = Vb[e];
+  }
+  int nv = (alg == DOA_ALG_MUSIC || alg == DOA_ALG_EV) ? Kn : 1;
+  if (lane < 16) ws[warp][lane] = 1.0;
+  if (alg == DOA_ALG_EV) {
+    const double lfloor = 100.0 * DBL_EPSILON * fmax(lb[M - 1], 0.0);
+    for (int j = 0; j < Kn; ++j) if (lb[j] <= lfloor) flag |= DOA_INFO_DEGENERATE;
+    if (lane < Kn) ws[warp][lane] = lb[lane] <= lfloor ? (lfloor > 0.0 ? 1.0 / lfloor : 1.0) : 1.0 / lb[lane];
+  }
+  __syncwarp();
+  if (alg == DOA_ALG_MN) {
+    double p0 = 0.0;
+    for (int j = 0; j < Kn; ++j) { const double2 v = U[j * ld]; p0 += v.x * v.x + v.y * v.y; }
+    const bool degen = !(p0 > 100.0 * DBL_EPSILON);
+    if (degen) flag |= DOA_INFO_DEGENERATE;
+    const double lp = degen ? 1.0 : 1.0 / p0;
+    double2 wv = make_double2(0.0, 0.0);
+    if (lane < M) {
+      double pr = 0.0, pi = 0.0;
+      for (int j = 0; j < Kn; ++j) {
+        const double2 e = U[j * ld + lane], e0 = U[j * ld];
+        pr += e.x * e0.x + e.y * e0.y;
+        pi += e.y * e0.x - e.x * e0.y;
+      }
+      wv = degen ? make_double2(pr, pi) : make_double2(pr * lp, pi * lp);
+    }
+    __syncwarp();
+    if (lane < M) U[lane] = wv;
+    __syncwarp();
+  }
+  const int npair = M * (M - 1) / 2;
+  for (int it = lane; it <= npair; it += 32) {
+    if (it == 0) {                                   // c_0 = trace C = sum_j w_j ||u_j||^2
+      double c0 = 0.0;
+      for (int j = 0; j < nv; ++j) {
+        double s = 0.0;
+        for (int p = 0; p < M; ++p) { const double2 x = U[j * ld + p]; s += x.x * x.x + x.y * x.y; }
+        c0 += ws[warp][j] * s;
+      }
+      coef[coef_index(b, 0, S)] = c0;
+    } else {
+      int p, q;
+      pair_of(it - 1, M, p, q);
+      double cr = 0.0, ci = 0.0;
+      for (int j = 0; j < nv; ++j) {
+        const double2 x = U[j * ld + p], y = U[j * ld + q];        // u[p] conj(u[q])
+        cr += ws[warp][j] * (x.x * y.x + x.y * y.y);
+        ci += ws[warp][j] * (x.y * y.x - x.x * y.y);
+      }
+      coef[coef_index(b, 2 * it - 1, S)] = 2.0 * cr;
+      coef[coef_index(b, 2 * it, S)] = -2.0 * ci;
+    }
+  }
+  for (int j = K + lane; j < 4 * S; j += 32) coef[coef_index(b, j, S)] = 0.0;
+  if (lane == 0) {
+    cnt[b] = 0;
+    if (info) info[b] |= flag;
+  }
+}
+
+template <int M>
+struct ArrShape {
+  static constexpr int K = 1 + M * (M - 1);
+  static constexpr int S = (K + 3) / 4;
+  static constexpr int NA = (64 / S) < 1 ? 1 : ((64 / S) > 8 ? 8 : (64 / S));
+  static constexpr int W = 8 * NA;             // angles per block (no halo: f is stored)
+  static constexpr int NB = 2;
+};
+constexpr int kArrWarps = 8;
+
+// table entry j of flattened grid point pt
+__device__ __forceinline__ double arr_entry(int j, int K, int64_t pt, const double* __restrict__ dpos, double az0,
+                                            double daz, double el0, double del, int64_t nel) {
+  if (j == 0) return 1.0;
+  if (j >= K) return 0.0;
+  const int64_t ia = pt / nel, ie = pt - (pt / nel) * nel;
+  const double az = __dadd_rn(__dmul_rn((double)ia, daz), az0);
+  const double el = __dadd_rn(__dmul_rn((double)ie, del), el0);
+  double saz, caz, sel, cel;
+  sincospi(az / 180.0, &saz, &caz);
+  sincospi(el / 180.0, &sel, &cel);
+  const int pr = (j - 1) >> 1;
+  const double arg = 2.0 * (dpos[3 * pr] * saz * sel + dpos[3 * pr + 1] * caz * sel + dpos[3 * pr + 2] * cel);
+  return (j & 1) ? cospi(arg) : sinpi(arg);       // z_pq = exp(j pi arg): (cos, sin) at j = (odd, even)
+}
+
+template <int M>
+__global__ void __launch_bounds__(kArrWarps * 32) scan_array_kernel(const double* __restrict__ coef, int64_t B,
+                                                                   int64_t per, const double* __restrict__ dpos,
+                                                                   double az0, double daz, double el0, double del,
+                                                                   int64_t nel, int64_t L, double* __restrict__ fbuf) {
+  using Sh = ArrShape<M>;
+  constexpr int K = Sh::K, S = Sh::S, NA = Sh::NA, W = Sh::W, NB = Sh::NB;
+  extern __shared__ double Ta[];                                   // [NB][S][NA][32]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane & 3, r = lane >> 2;
+  const int64_t col0 = (int64_t)blockIdx.x * NB * W;
+  for (int e = threadIdx.x; e < NB * S * NA * 32; e += kArrWarps * 32) {
+    const int ln = e & 31, t = (e >> 5) % NA, s = (e / (32 * NA)) % S, k = e / (32 * NA * S);
+    const int64_t pt = col0 + (int64_t)k * W + 8 * t + (ln >> 2);
+    const int j = 4 * s + (ln & 3);
+    Ta[e] = (pt < L) ? arr_entry(j, K, pt, dpos, az0, daz, el0, del, nel) : (j == 0 ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  const int64_t ngroups = (B + 7) / 8;
+  const int64_t g0 = (int64_t)blockIdx.y * per;
+  const int64_t g1 = (g0 + per < ngroups) ? g0 + per : ngroups;
+  for (int64_t g = g0 + warp; g < g1; g += kArrWarps) {
+    const double* cg = coef + ((size_t)g * S) * 32 + lane;
+    const int64_t b = g * 8 + r;
+#pragma unroll 1
+    for (int k = 0; k < NB; ++k) {
+      const int64_t base = col0 + (int64_t)k * W;
+      if (base >= L) break;
+      const double* Tk = Ta + (size_t)k * S * NA * 32 + lane;
+      double acc[NA][2];
+#pragma unroll
+      for (int t = 0; t < NA; ++t) { acc[t][0] = 0.0; acc[t][1] = 0.0; }
+#pragma unroll 4
+      for (int s = 0; s < S; ++s) {
+        const double a = __ldg(cg + s * 32);
+#pragma unroll
+        for (int t = 0; t < NA; ++t) dmma_a(acc[t][0], acc[t][1], a, Tk[(s * NA + t) * 32]);
+      }
+      if (b < B) {
+#pragma unroll
+        for (int t = 0; t < NA; ++t)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int64_t pt = base + 8 * t + 2 * q + e;
+            const double f = acc[t][e];
+            if (pt < L) fbuf[(size_t)b * L + pt] = f > kFloorA ? f : kFloorA;   // NaN -> floor (Q12)
+          }
+      }
+    }
+  }
+}
+
+// 2-D findPeaks (G2) on the floored f: thread per (frame, grid point).
+__global__ void peaks2d_kernel(const double* __restrict__ fbuf, int64_t B, int64_t naz, int64_t nel, int wrap,
+                               int cap, int32_t* __restrict__ cnt, int32_t* __restrict__ cidx,
+                               double* __restrict__ cf, float* __restrict__ P) {
+  const int64_t L = naz * nel;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < B * L; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / L, p = e - (e / L) * L;
+    const double* fb = fbuf + (size_t)b * L;
+    const double fp = fb[p];
+    if (P) P[e] = to_p32a(fp);
+    const int64_t ia = p / nel, ie = p - (p / nel) * nel;
+    bool peak = true;
+    for (int da = -1; da <= 1 && peak; ++da)
+      for (int de = -1; de <= 1 && peak; ++de) {
+        if (da == 0 && de == 0) continue;
+        int64_t ja = ia + da;
+        const int64_t je = ie + de;
+        if (je < 0 || je >= nel) continue;
+        if (ja < 0 || ja >= naz) {
+          if (!wrap) continue;
+          ja = (ja + naz) % naz;
+        }
+        const int64_t n = ja * nel + je;
+        if (n == p) continue;
+        const double fn = fb[n];
+        if (n < p ? !(fp < fn) : !(fp <= fn)) peak = false;
+      }
+    if (peak) {
+      const int slot = atomicAdd(cnt + b, 1);
+      if (slot < cap) {
+        cidx[(size_t)b * cap + slot] = (int32_t)p;
+        cf[(size_t)b * cap + slot] = fp;
+      }
+    }
+  }
+}
+
+template <int M>
+cudaError_t launch_scan_array_t(const doa_plan_s* p, int64_t B, cudaStream_t s) {
+  using Sh = ArrShape<M>;
+  const size_t smem = (size_t)Sh::NB * Sh::S * Sh::NA * 32 * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(scan_array_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const int64_t cols = (p->L + Sh::NB * Sh::W - 1) / (Sh::NB * Sh::W);
+  const int64_t ngroups = (B + 7) / 8;
+  int64_t per = (cols * ngroups) / (148 * 8);
+  if (per < 8) per = 8;
+  if (per > ngroups) per = ngroups;
+  const int64_t gy = (ngroups + per - 1) / per;
+  count_launch();
+  scan_array_kernel<M><<<dim3((unsigned)cols, (unsigned)gy), kArrWarps * 32, smem, s>>>(
+      p->coef, B, per, p->dpos, p->az0, p->daz, p->el0, p->del, p->nel, p->L, p->fbuf);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_array_spectrum(const doa_plan_s* p, const double* lam, const double* V, int64_t B, float* P,
+                                  int32_t* info, cudaStream_t s) {
+  count_launch();
+  coef_array_kernel<<<(unsigned)((B + 3) / 4), 128, 0, s>>>(lam, reinterpret_cast<const double2*>(V), B, p->M,
+                                                             p->D, p->alg, p->coef, p->cnt, info);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  switch (p->M) {
+#define DOA_ARR_CASE(m) case m: e = launch_scan_array_t<m>(p, B, s); break;
+    DOA_ARR_CASE(2) DOA_ARR_CASE(3) DOA_ARR_CASE(4) DOA_ARR_CASE(5) DOA_ARR_CASE(6) DOA_ARR_CASE(7)
+    DOA_ARR_CASE(8) DOA_ARR_CASE(9) DOA_ARR_CASE(10) DOA_ARR_CASE(11) DOA_ARR_CASE(12) DOA_ARR_CASE(13)
+    DOA_ARR_CASE(14) DOA_ARR_CASE(15) DOA_ARR_CASE(16)
+#undef DOA_ARR_CASE
+    default: return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  const int64_t tot = B * p->L;
+  int blocks = (int)((tot + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  count_launch();
+  peaks2d_kernel<<<blocks, 256, 0, s>>>(p->fbuf, B, p->naz, p->nel, p->wrap, p->cap, p->cnt, p->cand_idx,
+                                        p->cand_f, P);
+  return cudaGetLastError();
+}
+
+}  // namespace doa

@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "doa_internal.cuh"
 
@@ -64,6 +65,16 @@ cudaError_t ensure_run_scratch(doa_plan_s* p) {
     p->R = nullptr; p->lam = nullptr; p->V = nullptr;
   }
   return e;
+}
+
+// S3-S6 for either plan geometry: ULA -> Toeplitz coefficients + fused DMMA scan/peak test;
+// general array -> array coefficients + DMMA scan into the plan's f buffer + 2-D peak search.
+cudaError_t spectrum_stage(const doa_plan_s* p, const double* lam, const double* V, int64_t B, float* P,
+                           int32_t* info, cudaStream_t s) {
+  if (p->geom == 1) return doa::launch_array_spectrum(p, lam, V, B, P, info, s);
+  cudaError_t e = doa::launch_coef(p, lam, V, B, info, s);
+  if (e != cudaSuccess) return e;
+  return doa::launch_scan(p, B, P, s);
 }
 
 }  // namespace
@@ -131,9 +142,62 @@ doa_status_t doa_plan_create(doa_plan_t* plan, int32_t M, double d_over_lambda, 
   return DOA_OK;
 }
 
+doa_status_t doa_plan_create_array(doa_plan_t* plan, int32_t M, const double* positions, int32_t D, double az0_deg,
+                                   double daz_deg, int64_t naz, double el0_deg, double del_deg, int64_t nel,
+                                   int32_t az_wrap, int32_t alg, int64_t max_batch) {
+  g_launches = 0;
+  if (!plan) return fail(DOA_ERR_INVALID_ARG, "doa_plan_create_array: plan out-pointer is NULL");
+  *plan = nullptr;
+  if (M < 2) return fail(DOA_ERR_INVALID_ARG, "doa_plan_create_array: M=%d < 2", M);
+  if (M > 16) return fail(DOA_ERR_UNSUPPORTED, "doa_plan_create_array: M=%d > 16", M);
+  if (D < 1 || D >= M) return fail(DOA_ERR_INVALID_ARG, "doa_plan_create_array: D=%d outside [1, M-1]", D);
+  if (!positions) return fail(DOA_ERR_INVALID_ARG, "doa_plan_create_array: positions is NULL");
+  for (int i = 0; i < 3 * M; ++i)
+    if (!std::isfinite(positions[i])) return fail(DOA_ERR_INVALID_ARG, "doa_plan_create_array: non-finite position");
+  if (naz < 1 || nel < 1) return fail(DOA_ERR_INVALID_ARG, "doa_plan_create_array: naz, nel must be >= 1");
+  const int64_t L = naz * nel;
+  if (L < 3 || L >= (int64_t)1 << 31) return fail(DOA_ERR_INVALID_ARG, "doa_plan_create_array: L=%lld outside [3, 2^31)", (long long)L);
+  if (!std::isfinite(az0_deg) || !std::isfinite(el0_deg) || !std::isfinite(daz_deg) || !std::isfinite(del_deg) ||
+      (naz > 1 && !(daz_deg > 0.0)) || (nel > 1 && !(del_deg > 0.0)))
+    return fail(DOA_ERR_INVALID_ARG, "doa_plan_create_array: grid steps must be positive and finite");
+  if (alg < DOA_ALG_PHD || alg > DOA_ALG_MN) return fail(DOA_ERR_INVALID_ARG, "doa_plan_create_array: alg=%d", alg);
+  if (max_batch < 1) return fail(DOA_ERR_INVALID_ARG, "doa_plan_create_array: max_batch < 1");
+
+  doa_plan_s* p = new doa_plan_s();
+  std::memset(p, 0, sizeof *p);
+  p->M = M; p->D = D; p->alg = alg; p->geom = 1;
+  p->az0 = az0_deg; p->daz = daz_deg; p->naz = naz; p->el0 = el0_deg; p->del = del_deg; p->nel = nel;
+  p->wrap = az_wrap ? 1 : 0;
+  p->L = L; p->max_batch = max_batch;
+  p->cap = 128;
+  const int npair = M * (M - 1) / 2;
+  std::vector<double> dp((size_t)3 * (npair > 0 ? npair : 1));
+  for (int a = 0, k = 0; a < M; ++a)
+    for (int b = a + 1; b < M; ++b, ++k)
+      for (int c = 0; c < 3; ++c) dp[3 * k + c] = positions[3 * b + c] - positions[3 * a + c];   // r_q - r_p
+  const size_t B = (size_t)max_batch;
+  const size_t kw = (size_t)((max_batch + 7) / 8) * doa::array_ksteps(M) * 32;
+  cudaError_t e = cudaSuccess;
+  auto al = [&](void** ptr, size_t bytes) { if (e == cudaSuccess) e = cudaMalloc(ptr, bytes); };
+  al((void**)&p->cnt, B * sizeof(int32_t));
+  al((void**)&p->cand_idx, B * p->cap * sizeof(int32_t));
+  al((void**)&p->cand_f, B * p->cap * sizeof(double));
+  al((void**)&p->coef, kw * sizeof(double));
+  al((void**)&p->dpos, dp.size() * sizeof(double));
+  al((void**)&p->fbuf, B * (size_t)L * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemcpy(p->dpos, dp.data(), dp.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    doa_plan_destroy(p);
+    return cuda_fail(e, "doa_plan_create_array: workspace allocation");
+  }
+  *plan = p;
+  return DOA_OK;
+}
+
 doa_status_t doa_plan_destroy(doa_plan_t p) {
   if (!p) return DOA_OK;
   cudaDeviceSynchronize();
+  cudaFree(p->dpos); cudaFree(p->fbuf);
   cudaFree(p->cnt); cudaFree(p->cand_idx); cudaFree(p->cand_f); cudaFree(p->coef);
   cudaFree(p->R); cudaFree(p->lam); cudaFree(p->V);
   cudaFree(p->dX[0]); cudaFree(p->dX[1]); cudaFree(p->d_out);
@@ -184,8 +248,7 @@ doa_status_t doa_spectrum(doa_plan_t p, const double* lambda, const double* V, i
   DOA_CHECK_PTR(V, 16);
   DOA_CHECK_PTR(info, 4);
   if (P && !aligned(P, 4)) return fail(DOA_ERR_INVALID_ARG, "doa_spectrum: P is not 4-byte aligned");
-  DOA_TRY(doa::launch_coef(p, lambda, V, B, info, (cudaStream_t)s), "doa_spectrum/coef");
-  DOA_TRY(doa::launch_scan(p, B, P, (cudaStream_t)s), "doa_spectrum/scan");
+  DOA_TRY(spectrum_stage(p, lambda, V, B, P, info, (cudaStream_t)s), "doa_spectrum");
   p->last_B = B;
   return DOA_OK;
 }
@@ -224,8 +287,7 @@ doa_status_t doa_run(doa_plan_t p, const float* X, int64_t B, int64_t N, int32_t
   DOA_TRY(ensure_run_scratch(p), "doa_run: scratch allocation");
   DOA_TRY(doa::launch_covariance(X, B, N, p->M, p->R, st), "doa_run/covariance");
   DOA_TRY(doa::launch_eig(p->R, B, p->M, p->lam, p->V, info, st), "doa_run/eig");
-  DOA_TRY(doa::launch_coef(p, p->lam, p->V, B, info, st), "doa_run/coef");
-  DOA_TRY(doa::launch_scan(p, B, P, st), "doa_run/scan");
+  DOA_TRY(spectrum_stage(p, p->lam, p->V, B, P, info, st), "doa_run/spectrum");
   DOA_TRY(doa::launch_select(p, B, idx, val, npk, info, st), "doa_run/select");
   p->last_B = B;
   return DOA_OK;
@@ -305,8 +367,7 @@ doa_status_t doa_run_host(const doa_plan_t* plans, int32_t nplans, const float* 
     for (int a = 0; a < nplans; ++a) {
       doa_plan_s* q = plans[a];
       int32_t* inf = d_info + (size_t)a * B + b0;
-      DOA_TRY(doa::launch_coef(q, p->lam, p->V, nb, inf, st), "doa_run_host/coef");
-      DOA_TRY(doa::launch_scan(q, nb, nullptr, st), "doa_run_host/scan");
+      DOA_TRY(spectrum_stage(q, p->lam, p->V, nb, nullptr, inf, st), "doa_run_host/spectrum");
       DOA_TRY(doa::launch_select(q, nb, d_idx + ((size_t)a * B + b0) * D, d_val + ((size_t)a * B + b0) * D,
                                  d_npk + (size_t)a * B + b0, inf, st), "doa_run_host/select");
       q->last_B = 0;

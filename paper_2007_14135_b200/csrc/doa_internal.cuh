@@ -32,8 +32,16 @@ inline size_t coef_words(int64_t max_batch, int M) { return (size_t)((max_batch 
 
 struct doa_plan_s {
   int32_t M, D, alg, cap;
+  int32_t geom;                   // 0: ULA (Toeplitz scan); 1: general array on an az x el grid
   double dl, theta0, dtheta;
   int64_t L, max_batch;
+  // general-array plans (geom == 1): grid az_i = az0 + i daz (i < naz), el_j = el0 + j del (j < nel),
+  // flattened azimuth-major; element-pair position differences r_q - r_p (p < q) in wavelengths
+  double az0, daz, el0, del;
+  int64_t naz, nel;
+  int32_t wrap;
+  double* dpos;                   // [M(M-1)/2][3] device
+  double* fbuf;                   // [max_batch][L] floored f of the last doa_spectrum (device)
   int64_t last_B;                 // B of the last doa_spectrum (consumed by doa_peaks)
   // workspace (device)
   int32_t* cnt;                   // [max_batch]           candidate counters
@@ -63,6 +71,11 @@ cudaError_t launch_coef(const doa_plan_s* p, const double* lam, const double* V,
 cudaError_t launch_scan(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s);
 cudaError_t launch_select(const doa_plan_s* p, int64_t B, int32_t* idx, float* val, int32_t* npk, int32_t* info,
                           cudaStream_t s);
+// general-array plans (csrc/array.cu): coefficients, scan into fbuf, 2-D candidates (+ optional P)
+cudaError_t launch_array_spectrum(const doa_plan_s* p, const double* lam, const double* V, int64_t B, float* P,
+                                  int32_t* info, cudaStream_t s);
+__host__ __device__ constexpr int array_terms(int M) { return 1 + M * (M - 1); }   // c_0 + (Re, Im) per pair
+__host__ __device__ constexpr int array_ksteps(int M) { return (array_terms(M) + 3) / 4; }
 
 void count_launch();
 

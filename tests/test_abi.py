@@ -74,3 +74,20 @@ def test_binding_is_thin(lib):
     src = open(lib.binding.__file__).read()
     for bad in ("np.linalg", "torch.linalg", "torch.fft", "import oracle", "from oracle"):
         assert bad not in src
+
+
+@pytest.mark.parametrize("M,D,naz,nel,daz,dele,status", [
+    (1, 1, 360, 1, 1.0, 1.0, 1),      # M < 2
+    (17, 2, 360, 1, 1.0, 1.0, 2),     # M > 16: unsupported for general arrays
+    (8, 8, 360, 1, 1.0, 1.0, 1),      # D >= M
+    (8, 2, 1, 2, 1.0, 1.0, 1),        # L < 3
+    (8, 2, 360, 1, 0.0, 1.0, 1),      # daz <= 0 with naz > 1
+    (8, 2, 360, 2, 1.0, -1.0, 1),     # del <= 0 with nel > 1
+])
+def test_plan_create_array_validation(lib, M, D, naz, nel, daz, dele, status):
+    import numpy as np
+    pos = np.zeros((max(M, 1), 3))
+    h = C.c_void_p(7)
+    st = lib.lib.doa_plan_create_array(C.byref(h), M, pos.ctypes.data_as(C.POINTER(C.c_double)), D, 0.0, daz,
+                                       naz, 90.0, dele, nel, 1, 1, 1)
+    assert st == status and h.value is None
