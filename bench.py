@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay the step as a CUDA graph (auto: single-GPU runs)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle CPU time for cpu_baseline")
     return ap.parse_args()
 
@@ -176,6 +178,11 @@ def run_reference(args, cfg):
 
 
 def config_dict(cfg, frames_per_gpu, n_gpus):
+    if hasattr(cfg, "naz"):                        # general array (NEXT-1)
+        return {"workload": cfg.name, "frames_per_gpu": frames_per_gpu, "global_batch": frames_per_gpu * n_gpus,
+                "M": cfg.M, "N": cfg.N, "D": cfg.D, "geometry": "UCA r=10 m @ 15 MHz (Eq. 2)" if cfg.M == 8 else "array",
+                "grid": f"{cfg.naz} az x {cfg.nel} el", "L": cfg.L, "snr_db": cfg.snr_db, "algs": list(ALGS),
+                "parallelism": f"frames sharded dp{n_gpus}"}
     return {"workload": cfg.name, "frames_per_gpu": frames_per_gpu, "global_batch": frames_per_gpu * n_gpus,
             "M": cfg.M, "N": cfg.N, "D": cfg.D, "L": cfg.L, "dtheta_deg": cfg.dtheta, "d_over_lambda": cfg.d_over_lambda,
             "snr_db": cfg.snr_db, "algs": list(ALGS), "parallelism": f"frames sharded dp{n_gpus}",
@@ -187,8 +194,16 @@ def config_dict(cfg, frames_per_gpu, n_gpus):
 def main():
     args = parse()
     from synth import get_config
-    cfg = get_config(args.workload)
+    from synth.array import ARRAY_CONFIGS, generate_array
+    is_array = args.workload in ARRAY_CONFIGS       # general geometry (NEXT-1: the paper's UCA workload)
+    cfg = ARRAY_CONFIGS[args.workload] if is_array else get_config(args.workload)
+    if is_array and os.environ.get("DOA_BENCH_NEL"):   # the paper's 360 x {1, 30, 60, 90} sweep
+        nel = int(os.environ["DOA_BENCH_NEL"])
+        cfg = cfg.with_(name=f"e1_360x{nel}", el0=90.0 if nel == 1 else 1.0, nel=nel)
     if args.impl == "reference":
+        if is_array:
+            print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for ULA workloads"}))
+            return
         return run_reference(args, cfg)
 
     ws, rank, local = dist_env()
@@ -197,7 +212,7 @@ def main():
     # generate this rank's frames BEFORE touching CUDA (the generator forks worker processes)
     from synth import generate
     t0 = time.perf_counter()
-    Xh_np = generate(cfg, frames=frames)
+    Xh_np = generate_array(cfg, frames=frames) if is_array else generate(cfg, frames=frames)
     gen_s = time.perf_counter() - t0
 
     import torch
@@ -214,8 +229,12 @@ def main():
     del Xh_np
     X = Xh.to(dev)
     M, D, L = cfg.M, cfg.D, cfg.L
-    plans = [doa.Plan(M, D, a, cfg.dtheta, L=L, theta0=cfg.theta0, d_over_lambda=cfg.d_over_lambda,
-                      max_batch=B, device=dev) for a in ALGS]
+    if is_array:
+        plans = [doa.Plan.array(cfg.pos, D, a, cfg.az0, cfg.daz, cfg.naz, cfg.el0, cfg.del_, cfg.nel, cfg.az_wrap,
+                                max_batch=B, device=dev) for a in ALGS]
+    else:
+        plans = [doa.Plan(M, D, a, cfg.dtheta, L=L, theta0=cfg.theta0, d_over_lambda=cfg.d_over_lambda,
+                          max_batch=B, device=dev) for a in ALGS]
     R = torch.empty((B, M, M), dtype=torch.complex128, device=dev)
     lam = torch.empty((B, M), dtype=torch.float64, device=dev)
     V = torch.empty((B, M, M), dtype=torch.complex128, device=dev)
@@ -232,11 +251,12 @@ def main():
     s = stream.cuda_stream
     spec_ev = []   # (start, end) events around each doa_spectrum call (coefficients + scan kernel)
 
-    def step(record=False):
+    def step(sh, record=False):
+        """One step on stream handle `sh`; returns the number of libdoa kernel launches."""
         launches = 0
-        bd.doa_covariance(plans[0].h, X, R, s)
+        bd.doa_covariance(plans[0].h, X, R, sh)
         launches += bd.doa_last_launch_count()
-        bd.doa_eig(plans[0].h, R, lam, V, info_eig, s)
+        bd.doa_eig(plans[0].h, R, lam, V, info_eig, sh)
         launches += bd.doa_last_launch_count()
         for a, p in enumerate(plans):
             info[a].copy_(info_eig)
@@ -244,21 +264,37 @@ def main():
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-            bd.doa_spectrum(p.h, lam, V, info[a], None, s)
+            bd.doa_spectrum(p.h, lam, V, info[a], None, sh)
             launches += bd.doa_last_launch_count()
             if record:
                 e1.record(stream)
                 spec_ev.append((e0, e1))
-            bd.doa_peaks(p.h, B, idx[a], val[a], npk[a], info[a], s)
+            bd.doa_peaks(p.h, B, idx[a], val[a], npk[a], info[a], sh)
             launches += bd.doa_last_launch_count()
         if ws > 1:
             pdist.pack_peaks(idx, val, npk, info, out=packed)
             pdist.gather_peaks(packed, out=gathered)
         return launches
 
+    # CUDA graph: the step is a fixed sequence of async ABI calls on one stream, so it can be
+    # captured once and replayed (removes the ~10 us per-launch CPU overhead that dominates
+    # single-frame workloads).  Default: on for single-GPU runs.
+    use_graph = args.graph == "on" or (args.graph == "auto" and ws == 1)
     for _ in range(max(3, args.warmup)):
-        step()
+        step(s)
     torch.cuda.synchronize()
+    graph = None
+    launches_per_step = 0
+    if use_graph:
+        for _ in range(min(args.steps, 5)):           # per-launch timing of doa_spectrum, outside the graph
+            step(s, record=True)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            launches_per_step = step(torch.cuda.current_stream().cuda_stream)
+        for _ in range(max(3, args.warmup)):
+            graph.replay()
+        torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -270,7 +306,11 @@ def main():
     ev0.record(stream)
     launches = 0
     for _ in range(args.steps):
-        launches += step(record=True)
+        if graph is not None:
+            graph.replay()
+            launches += launches_per_step
+        else:
+            launches += step(s, record=True)
     ev1.record(stream)
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
@@ -286,7 +326,10 @@ def main():
 
     # roofline of the dominant kernel: the scan (S4-S6) inside doa_spectrum
     spec_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in spec_ev)
-    scan_flops = 4.0 * (M - 1) * L * B            # 2(M-1) fp64 FMAs per (frame, angle)
+    if is_array:                                   # K - 1 = M(M-1) fp64 FMAs per (frame, grid point)
+        scan_flops = 2.0 * M * (M - 1) * L * B
+    else:                                          # 2(M-1) fp64 FMAs per (frame, angle)
+        scan_flops = 4.0 * (M - 1) * L * B
     pk = peaks_json()
     fp64_peak = 148 * 64 * 2 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12   # TFLOP/s, guide unit counts
     achieved = scan_flops / (spec_ms / 1e3) / 1e12
@@ -341,7 +384,7 @@ def main():
                "api": "doa_run_host (4 plans)", "matches_device_path": same}
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not is_array:
         cpu = oracle_baseline(cfg, args.cpu_seconds)
 
     if rank == 0:
@@ -351,7 +394,7 @@ def main():
                 "config": config_dict(cfg, B, ws),
                 "points_per_s": value * L * len(ALGS),
                 "roofline": roofline, "cpu_baseline": cpu, "clocks": clk, "e2e": e2e,
-                "gpu_launches": launches, "gen_seconds": gen_s}
+                "gpu_launches": launches, "cuda_graph": bool(use_graph), "gen_seconds": gen_s}
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
