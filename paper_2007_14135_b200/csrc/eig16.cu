@@ -171,12 +171,22 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
         const double ir = rsqrt(rot ? r2 : 1.0);              // 1/|a_xy|
         const double rr = r2 * ir;                            // |a_xy|
         const double tau = (ayy - axx) * (0.5 * ir);
+#if DOA_EIG_F32_ANGLE
+        // The rotation ANGLE only needs to be close to the zeroing one: t is computed in fp32
+        // (short MUFU latency), then c = 1/sqrt(1 + t^2), s = t c in fp64 keep J exactly unitary,
+        // and the 2x2 diagonal block is rotated explicitly (its tiny off-diagonal remainder stays
+        // in A and is removed by later sweeps; same stop rule).
+        const float atf = fabsf((float)tau);
+        float tf = __frcp_rn(atf > 1e18f ? 2.0f * atf : atf + __fsqrt_rn(fmaf(atf, atf, 1.0f)));
+        double t = rot ? (tau < 0.0 ? -(double)tf : (double)tf) : 0.0;
+#else
         const double at = fabs(tau);
         const double atc = fmin(at, 1e150);
         const double w = fma(atc, atc, 1.0);
         // 1/(|tau| + sqrt(1 + tau^2)); -> 1/(2|tau|) once tau^2 would overflow
         double t = __drcp_rn(at > 1e150 ? 2.0 * at : atc + w * rsqrt(w));
         t = rot ? (tau < 0.0 ? -t : t) : 0.0;
+#endif
         Prm p;
         p.c = rot ? rsqrt(fma(t, t, 1.0)) : 1.0;
         p.s = t * p.c;
@@ -184,9 +194,18 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
         p.ei = rot ? -axy.y * ir : 0.0;
         if (lane < 8) {
           prm[warp][lane] = p;
+#if DOA_EIG_F32_ANGLE
+          const double cc = p.c * p.c, ss = p.s * p.s, cs = p.c * p.s;
+          An[wxx] = make_double2(cc * axx - 2.0 * cs * rr + ss * ayy, 0.0);
+          An[wyy] = make_double2(ss * axx + 2.0 * cs * rr + cc * ayy, 0.0);
+          // (G^T B G)_12 = cs (a_xx - a_yy) + (c^2 - s^2) |a_xy|, real in the rotated basis; stored at
+          // (min, max) of the permuted pair, conjugation of a real value is a no-op
+          An[wxy] = make_double2(cs * (axx - ayy) + (cc - ss) * rr, 0.0);
+#else
           An[wxx] = make_double2(axx - t * rr, 0.0);
           An[wyy] = make_double2(ayy + t * rr, 0.0);
           An[wxy] = make_double2(0.0, 0.0);
+#endif
         }
       }
       __syncwarp();
