@@ -64,6 +64,25 @@ __device__ __forceinline__ int cat_next(int s) {
   return (s & 1) ? s - 2 : s + 2;
 }
 
+// Branch-free reciprocal (square root) for positive normal arguments: MUFU seed (rsqrt/rcp
+// .approx.ftz.f64) + two Newton steps, ~1 ulp.  The library versions add special-case branches
+// that cost a third of the rotation-parameter instructions.
+__device__ __forceinline__ double rsqrt_pos(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+__device__ __forceinline__ double rcp_pos(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-x, y, 2.0);
+  y = y * fma(-x, y, 2.0);
+  return y;
+}
+
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
@@ -167,8 +186,8 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
         const double2 axy = A[rxy];
         const double axx = A[rxx].x, ayy = A[ryy].x;
         const double r2 = axy.x * axy.x + axy.y * axy.y;
-        const bool rot = r2 != 0.0;                           // a_xy == 0: identity rotation
-        const double ir = rsqrt(rot ? r2 : 1.0);              // 1/|a_xy|
+        const bool rot = r2 > 1e-300;                         // a_xy ~ 0: identity rotation
+        const double ir = rsqrt_pos(rot ? r2 : 1.0);          // 1/|a_xy|
         const double rr = r2 * ir;                            // |a_xy|
         const double tau = (ayy - axx) * (0.5 * ir);
 #if DOA_EIG_F32_ANGLE
@@ -184,11 +203,11 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
         const double atc = fmin(at, 1e150);
         const double w = fma(atc, atc, 1.0);
         // 1/(|tau| + sqrt(1 + tau^2)); -> 1/(2|tau|) once tau^2 would overflow
-        double t = __drcp_rn(at > 1e150 ? 2.0 * at : atc + w * rsqrt(w));
+        double t = rcp_pos(fmin(at > 1e150 ? 2.0 * at : atc + w * rsqrt_pos(w), 1e300));
         t = rot ? (tau < 0.0 ? -t : t) : 0.0;
 #endif
         Prm p;
-        p.c = rot ? rsqrt(fma(t, t, 1.0)) : 1.0;
+        p.c = rot ? rsqrt_pos(fma(t, t, 1.0)) : 1.0;
         p.s = t * p.c;
         p.er = rot ? axy.x * ir : 1.0;
         p.ei = rot ? -axy.y * ir : 0.0;

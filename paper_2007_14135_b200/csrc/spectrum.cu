@@ -168,22 +168,28 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 constexpr int kCtaWarps = 8;
 constexpr long long kInfBits = 0x7FF0000000000000LL;        // bits of +inf
 constexpr long long kFloorBits = 0x01A56E1FC2F8F359LL;      // bits of 1e-300 (kFloor, Q12)
-constexpr int kNB = 2;                                       // angle blocks per column
 
-template <int M>
+// Shape by k-steps S = ceil((2M-1)/4) (M <= 64 -> S <= 32): 8 tiles of 8 angles per block; S <= 8
+// (M <= 16) keeps the A fragments of a group in registers with a one-group prefetch and uses two
+// blocks per column; larger S streams the A fragment of each k-step from L1/L2 and uses one block
+// (table: S x 8 x 32 doubles = up to 64 KB of smem).
+template <int S>
 struct ScanShape {
-  static constexpr int S = (2 * M + 3) / 4;                 // k-steps of 4 (K = 4S >= 2M-1)
-  static constexpr int NA = (64 / S) < 8 ? (64 / S) : 8;    // 8-angle tiles per block
+  static constexpr int NA = 8;                               // 8-angle tiles per block
   static constexpr int W = 8 * NA;                           // angles per block (incl. 2 halo)
+  static constexpr bool STREAM_A = S > 8;
+  static constexpr int NB = STREAM_A ? 1 : 2;                // blocks per column
 };
 
-template <int M, bool WRITE_P>
-__global__ void __launch_bounds__(kCtaWarps * 32, 2) scan_cta_kernel(const double* __restrict__ coef, int64_t B,
+template <int S, bool WRITE_P>
+__global__ void __launch_bounds__(kCtaWarps * 32, 2) scan_cta_kernel(const double* __restrict__ coef, int64_t B, int M,
                                                                    int64_t per, double dl, double theta0, double dtheta, int L,
                                                                    int cap, int32_t* __restrict__ cnt,
                                                                    int32_t* __restrict__ cidx,
                                                                    double* __restrict__ cf, float* __restrict__ P) {
-  constexpr int S = ScanShape<M>::S, NA = ScanShape<M>::NA, W = ScanShape<M>::W, NB = kNB;
+  constexpr int NA = ScanShape<S>::NA, W = ScanShape<S>::W, NB = ScanShape<S>::NB;
+  constexpr bool STREAM_A = ScanShape<S>::STREAM_A;
+  constexpr int SA = STREAM_A ? 1 : S;                           // register-held A fragments
   extern __shared__ double Ts[];                                 // [NB][S][NA][32]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q = lane & 3, r = lane >> 2;
@@ -204,20 +210,23 @@ __global__ void __launch_bounds__(kCtaWarps * 32, 2) scan_cta_kernel(const doubl
     __syncthreads();
     const int64_t g0 = y * per;
     const int64_t g1 = (g0 + per < ngroups) ? g0 + per : ngroups;
-    double an[S];
-    if (g0 + warp < g1) {
+    double an[SA];
+    if (!STREAM_A && g0 + warp < g1) {
       const double* cg = coef + ((size_t)(g0 + warp) * S) * 32 + lane;
 #pragma unroll
-      for (int s = 0; s < S; ++s) an[s] = __ldg(cg + s * 32);
+      for (int s = 0; s < SA; ++s) an[s] = __ldg(cg + s * 32);
     }
     for (int64_t g = g0 + warp; g < g1; g += kCtaWarps) {
-      double a[S];
+      const double* cgc = coef + ((size_t)g * S) * 32 + lane;   // this group's A fragments
+      double a[SA];
+      if (!STREAM_A) {
 #pragma unroll
-      for (int s = 0; s < S; ++s) a[s] = an[s];
-      if (g + kCtaWarps < g1) {                                  // prefetch the next group's operands
-        const double* cg = coef + ((size_t)(g + kCtaWarps) * S) * 32 + lane;
+        for (int s = 0; s < SA; ++s) a[s] = an[s];
+        if (g + kCtaWarps < g1) {                                // prefetch the next group's operands
+          const double* cg = coef + ((size_t)(g + kCtaWarps) * S) * 32 + lane;
 #pragma unroll
-        for (int s = 0; s < S; ++s) an[s] = __ldg(cg + s * 32);
+          for (int s = 0; s < SA; ++s) an[s] = __ldg(cg + s * 32);
+        }
       }
       const int b = (int)(g * 8) + r;
       const bool frame_ok = b < B;
@@ -230,9 +239,11 @@ __global__ void __launch_bounds__(kCtaWarps * 32, 2) scan_cta_kernel(const doubl
 #pragma unroll
         for (int t = 0; t < NA; ++t) { acc[t][0] = 0.0; acc[t][1] = 0.0; }
 #pragma unroll
-        for (int s = 0; s < S; ++s)
+        for (int s = 0; s < S; ++s) {
+          const double av = STREAM_A ? __ldg(cgc + s * 32) : a[STREAM_A ? 0 : s];
 #pragma unroll
-          for (int t = 0; t < NA; ++t) dmma_884(acc[t][0], acc[t][1], a[s], Tk[(s * NA + t) * 32]);
+          for (int t = 0; t < NA; ++t) dmma_884(acc[t][0], acc[t][1], av, Tk[(s * NA + t) * 32]);
+        }
         // Fast path: if every value of the warp's tile is a positive double above the floor and
         // not NaN (checked on the high words, conservatively), the raw bits already are the
         // floored values; otherwise the whole tile takes the explicit floor, which maps negative
@@ -309,50 +320,6 @@ __global__ void __launch_bounds__(kCtaWarps * 32, 2) scan_cta_kernel(const doubl
   }
 }
 
-// Same contraction for 32 < M <= 64 with the table in shared memory and plain DFMA (runtime M;
-// a register/B-fragment table of K = 4S <= 128 entries per angle would not pay off there).
-// Lanes own angles of a 32-angle block with halo lanes 0 and 31 (stride 30).
-constexpr int kSmemWarps = 4;
-constexpr int kSmemStride = 30;
-
-__global__ void __launch_bounds__(kSmemWarps * 32) scan_smem_kernel(const double* __restrict__ coef, int64_t B, int M,
-                                                                   int64_t frames_per_cta, double dl, double theta0,
-                                                                   double dtheta, int64_t L, int cap,
-                                                                   int32_t* __restrict__ cnt,
-                                                                   int32_t* __restrict__ cidx, double* __restrict__ cf,
-                                                                   float* __restrict__ P) {
-  extern __shared__ double tsm[];
-  const int S = ksteps(M);
-  const int NJ = 4 * S;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* T = tsm + (size_t)warp * NJ * 32;          // T[j][lane]
-  const int64_t wblk = (int64_t)blockIdx.x * kSmemWarps + warp;
-  const int64_t i = wblk * kSmemStride - 1 + lane;
-  const bool valid = (i >= 0 && i < L);
-  const double u = valid ? grid_u(i, theta0, dtheta, dl) : 0.0;
-  for (int j = 0; j < NJ; ++j) T[j * 32 + lane] = valid ? table_entry(j, M, u) : (j == 0 ? 1.0 : 0.0);
-  __syncwarp();
-  const bool own = lane >= 1 && lane <= kSmemStride && valid;
-  const bool decide = own && i >= 1 && i <= L - 2;
-  const int64_t b0 = (int64_t)blockIdx.y * frames_per_cta;
-  const int64_t b1 = (b0 + frames_per_cta < B) ? b0 + frames_per_cta : B;
-  for (int64_t b = b0; b < b1; ++b) {
-    double acc = __ldg(coef + coef_index(b, 0, S));
-    for (int j = 1; j < 2 * M - 1; ++j) acc = fma(__ldg(coef + coef_index(b, j, S)), T[j * 32 + lane], acc);
-    const double f = acc > kFloor ? acc : kFloor;
-    const double fl = __shfl_up_sync(0xffffffffu, f, 1);
-    const double fr = __shfl_down_sync(0xffffffffu, f, 1);
-    if (decide && f < fl && f <= fr) {
-      const int slot = atomicAdd(cnt + b, 1);
-      if (slot < cap) {
-        cidx[(size_t)b * cap + slot] = (int32_t)i;
-        cf[(size_t)b * cap + slot] = f;
-      }
-    }
-    if (P && own) P[(size_t)b * L + i] = to_p32(f);
-  }
-}
-
 int sm_count() {
   static int n = 0;
   if (!n) {
@@ -364,15 +331,15 @@ int sm_count() {
   return n;
 }
 
-template <int M>
+template <int S>
 cudaError_t launch_scan_cta(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
-  constexpr int S = ScanShape<M>::S, NA = ScanShape<M>::NA, W = ScanShape<M>::W, NB = kNB;
+  constexpr int NA = ScanShape<S>::NA, W = ScanShape<S>::W, NB = ScanShape<S>::NB;
   const size_t smem = (size_t)NB * S * NA * 32 * sizeof(double);
   static int occ = 0;
   if (!occ) {
-    cudaFuncSetAttribute(scan_cta_kernel<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(scan_cta_kernel<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_cta_kernel<M, false>, kCtaWarps * 32, smem);
+    cudaFuncSetAttribute(scan_cta_kernel<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(scan_cta_kernel<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_cta_kernel<S, false>, kCtaWarps * 32, smem);
     if (occ < 1) occ = 1;
   }
   const int64_t nwb = (p->L + (W - 2) - 1) / (W - 2);           // angle blocks owning [0, L)
@@ -387,31 +354,12 @@ cudaError_t launch_scan_cta(const doa_plan_s* p, int64_t B, float* P, cudaStream
   const dim3 grid((unsigned)gx, (unsigned)gy);
   count_launch();
   if (P)
-    scan_cta_kernel<M, true><<<grid, kCtaWarps * 32, smem, s>>>(p->coef, B, per, p->dl, p->theta0, p->dtheta,
+    scan_cta_kernel<S, true><<<grid, kCtaWarps * 32, smem, s>>>(p->coef, B, p->M, per, p->dl, p->theta0, p->dtheta,
                                                                (int)p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
   else
-    scan_cta_kernel<M, false><<<grid, kCtaWarps * 32, smem, s>>>(p->coef, B, per, p->dl, p->theta0, p->dtheta,
-                                                                (int)p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_scan_smem(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
-  const int64_t nwb = (p->L + kSmemStride - 1) / kSmemStride;
-  const int64_t gx = (nwb + kSmemWarps - 1) / kSmemWarps;
-  int64_t fpc = (gx * B) / (148 * 2 * 8);
-  if (fpc < 16) fpc = 16;
-  if (fpc > B) fpc = B;
-  const int64_t gy = (B + fpc - 1) / fpc;
-  const size_t smem = (size_t)kSmemWarps * 4 * ksteps(p->M) * 32 * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(scan_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(kSmemWarps * 4 * ksteps(kMaxM) * 32 * sizeof(double)));
-    attr = true;
-  }
-  count_launch();
-  scan_smem_kernel<<<dim3((unsigned)gx, (unsigned)gy), kSmemWarps * 32, smem, s>>>(
-      p->coef, B, p->M, fpc, p->dl, p->theta0, p->dtheta, p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
+    scan_cta_kernel<S, false><<<grid, kCtaWarps * 32, smem, s>>>(p->coef, B, p->M, per, p->dl, p->theta0,
+                                                                p->dtheta, (int)p->L, p->cap, p->cnt, p->cand_idx,
+                                                                p->cand_f, P);
   return cudaGetLastError();
 }
 
@@ -475,16 +423,16 @@ cudaError_t launch_coef(const doa_plan_s* p, const double* lam, const double* V,
 }
 
 cudaError_t launch_scan(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
-  switch (p->M) {
-#define DOA_SCAN_CASE(m) case m: return launch_scan_cta<m>(p, B, P, s);
-    DOA_SCAN_CASE(2) DOA_SCAN_CASE(3) DOA_SCAN_CASE(4) DOA_SCAN_CASE(5) DOA_SCAN_CASE(6) DOA_SCAN_CASE(7)
-    DOA_SCAN_CASE(8) DOA_SCAN_CASE(9) DOA_SCAN_CASE(10) DOA_SCAN_CASE(11) DOA_SCAN_CASE(12) DOA_SCAN_CASE(13)
-    DOA_SCAN_CASE(14) DOA_SCAN_CASE(15) DOA_SCAN_CASE(16) DOA_SCAN_CASE(17) DOA_SCAN_CASE(18) DOA_SCAN_CASE(19)
-    DOA_SCAN_CASE(20) DOA_SCAN_CASE(21) DOA_SCAN_CASE(22) DOA_SCAN_CASE(23) DOA_SCAN_CASE(24)
-    DOA_SCAN_CASE(25) DOA_SCAN_CASE(26) DOA_SCAN_CASE(27) DOA_SCAN_CASE(28) DOA_SCAN_CASE(29)
-    DOA_SCAN_CASE(30) DOA_SCAN_CASE(31) DOA_SCAN_CASE(32)
+  switch (ksteps(p->M)) {
+#define DOA_SCAN_CASE(k) case k: return launch_scan_cta<k>(p, B, P, s);
+    DOA_SCAN_CASE(1) DOA_SCAN_CASE(2) DOA_SCAN_CASE(3) DOA_SCAN_CASE(4) DOA_SCAN_CASE(5) DOA_SCAN_CASE(6)
+    DOA_SCAN_CASE(7) DOA_SCAN_CASE(8) DOA_SCAN_CASE(9) DOA_SCAN_CASE(10) DOA_SCAN_CASE(11) DOA_SCAN_CASE(12)
+    DOA_SCAN_CASE(13) DOA_SCAN_CASE(14) DOA_SCAN_CASE(15) DOA_SCAN_CASE(16) DOA_SCAN_CASE(17) DOA_SCAN_CASE(18)
+    DOA_SCAN_CASE(19) DOA_SCAN_CASE(20) DOA_SCAN_CASE(21) DOA_SCAN_CASE(22) DOA_SCAN_CASE(23) DOA_SCAN_CASE(24)
+    DOA_SCAN_CASE(25) DOA_SCAN_CASE(26) DOA_SCAN_CASE(27) DOA_SCAN_CASE(28) DOA_SCAN_CASE(29) DOA_SCAN_CASE(30)
+    DOA_SCAN_CASE(31) DOA_SCAN_CASE(32)
 #undef DOA_SCAN_CASE
-    default: return launch_scan_smem(p, B, P, s);
+    default: return cudaErrorInvalidValue;
   }
 }
 
