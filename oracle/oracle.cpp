@@ -183,15 +183,31 @@ Subspace noise_subspace(int alg, int M, int D, const std::vector<double>& lam, c
   return S;
 }
 
-// Table 2 Step-5 on the ULA grid: theta_i = theta0 + i*dtheta (multiply
-// then add, no FMA), u_i = 2 (d/lambda) sin(theta_i * pi/180), a_m = exp(-j pi m u_i) formed per
-// element (no recurrence).  invP = a^H C a evaluated as the sum of squares
-// sum_k w_k |u_k^H a|^2 (identical to a^H (sum_k w_k u_k u_k^H) a), floored at 1e-300 (Q12).
-void spectrum(const Subspace& S, int M, double dl, double theta0, double dtheta, int64_t i0, int64_t i1, double* f) {
+// Grid angle theta_i (Q26): theta0 + i*dtheta (rounded multiply, then
+// rounded add, no FMA).  When the grid is symmetric about 0 — its last point computed that way is
+// exactly -theta0, as for every -a:d:a grid of the paper ("-90:0.01:90") — the upper half
+// is built from the other end, theta_i = -theta_{L-1-i} for i >= H = ceil(L/2), so the computed
+// grid is exactly symmetric like the mathematical one (MATLAB's colon also builds a:d:b from
+// both ends).
+bool grid_symmetric(double theta0, double dtheta, int64_t L) {
+  return L >= 2 && theta0 + (double)(L - 1) * dtheta == -theta0;
+}
+double grid_theta(double theta0, double dtheta, int64_t L, bool sym, int64_t i) {
+  if (sym && i >= (L + 1) / 2) return -(theta0 + (double)(L - 1 - i) * dtheta);
+  return theta0 + (double)i * dtheta;
+}
+
+// Table 2 Step-5 on the ULA grid: theta_i as grid_theta,
+// u_i = 2 (d/lambda) sin(theta_i * pi/180), a_m = exp(-j pi m u_i) formed per element (no
+// recurrence).  invP = a^H C a evaluated as the sum of squares sum_k w_k |u_k^H a|^2 (identical
+// to a^H (sum_k w_k u_k u_k^H) a), floored at 1e-300 (Q12).
+void spectrum(const Subspace& S, int M, double dl, double theta0, double dtheta, int64_t L, int64_t i0, int64_t i1,
+              double* f) {
   const double pi = 3.14159265358979323846;
+  const bool sym = grid_symmetric(theta0, dtheta, L);
   std::vector<cd> a(M);
   for (int64_t i = i0; i < i1; ++i) {
-    const double th = theta0 + (double)i * dtheta;
+    const double th = grid_theta(theta0, dtheta, L, sym, i);
     const double u = 2.0 * dl * std::sin(th * pi / 180.0);
     for (int m = 0; m < M; ++m) {
       const double ph = pi * (double)m * u;
@@ -350,12 +366,12 @@ void oracle_spectrum(int alg, int M, int D, double dl, const double* lam, const 
   int inf = 0;
   Subspace S = noise_subspace(alg, M, D, l, unpack(V, (size_t)M * M), &inf);
   if (nthreads <= 1) {
-    spectrum(S, M, dl, theta0, dtheta, 0, L, f);
+    spectrum(S, M, dl, theta0, dtheta, L, 0, L, f);
   } else {
     std::vector<std::thread> th;
     for (int t = 0; t < nthreads; ++t) {
       const int64_t a = L * t / nthreads, b = L * (t + 1) / nthreads;
-      th.emplace_back([&, a, b] { spectrum(S, M, dl, theta0, dtheta, a, b, f); });
+      th.emplace_back([&, a, b] { spectrum(S, M, dl, theta0, dtheta, L, a, b, f); });
     }
     for (auto& x : th) x.join();
   }
@@ -382,7 +398,7 @@ void oracle_run_batch(int alg, int M, int D, double dl, double theta0, double dt
       covariance(X + (size_t)b * N * M * 2, N, M, R);
       const int sw = eig(R, M, lam, V, &inf);
       Subspace S = noise_subspace(alg, M, D, lam, V, &inf);
-      spectrum(S, M, dl, theta0, dtheta, 0, L, f.data());
+      spectrum(S, M, dl, theta0, dtheta, L, 0, L, f.data());
       peaks(f.data(), L, D, idx + b * D, fv.data(), npk + b);
       for (int k = 0; k < D; ++k) val[b * D + k] = k < npk[b] ? to_p32(fv[k]) : 0.0f;
       if (npk[b] < D) inf |= INFO_UNDERDETERMINED;

@@ -18,9 +18,18 @@ EPS = np.finfo(float).eps
 ALGS = ["phd", "music", "ev", "mn"]
 
 
-def _grid_u(theta0, dtheta, L, dl=0.5):
+def _grid_theta(theta0, dtheta, L):
+    """Q8 + Q26: theta0 + i*dtheta; a grid whose last point is exactly -theta0 is mirrored,
+    theta_i = -theta_{L-1-i} for i >= ceil(L/2)."""
     th = theta0 + np.arange(L) * dtheta
-    return 2 * dl * np.sin(np.deg2rad(th))
+    if L >= 2 and th[-1] == -theta0:
+        H = (L + 1) // 2
+        th[H:] = -th[: L - H][::-1]
+    return th
+
+
+def _grid_u(theta0, dtheta, L, dl=0.5):
+    return 2 * dl * np.sin(np.deg2rad(_grid_theta(theta0, dtheta, L)))
 
 
 def _noisy_R(orc, cfg, frame=0):
@@ -181,3 +190,36 @@ def test_ev_degenerate_flag(orc):
     f, info = orc.spectrum("ev", 1, 0.5, lam, V, -90.0, 1.0, 181)
     assert info & orc.INFO_DEGENERATE
     assert np.all(np.isfinite(f))
+
+
+@pytest.mark.parametrize("L,dth", [(18001, 0.01), (1801, 0.1), (180001, 0.001)])
+def test_symmetric_grid_mirror_pin(orc, L, dth):
+    # Q26: on a symmetric grid theta_{L-1-i} = -theta_i exactly, so for a REAL covariance
+    # (a(-u) = conj a(u), real eigenvectors) f is exactly even: f[i] == f[L-1-i] bit for bit.
+    # The plain formula theta0 + i*dtheta misses this in the last bits at thousands of indices.
+    th_plain = -90.0 + np.arange(L) * dth
+    assert np.any(th_plain != -th_plain[::-1])
+    th = _grid_theta(-90.0, dth, L)
+    assert np.array_equal(th, -th[::-1])
+    cfg = get_config("c2")
+    R = _noisy_R(orc, cfg).real.astype(complex)
+    lam, V, _, _ = orc.eig(R)
+    assert np.all(V.imag == 0)
+    for alg in ALGS:
+        f, _ = orc.spectrum(alg, cfg.D, 0.5, lam, V, -90.0, dth, L, threads=8)
+        assert np.array_equal(f, f[::-1]), alg
+
+
+def test_nonsymmetric_grid_is_plain(orc):
+    # a grid that does not end at -theta0 keeps theta0 + i*dtheta everywhere: compare with the
+    # brute-force a^H C a on that grid
+    cfg = get_config("c2")
+    lam, V, _, _ = orc.eig(_noisy_R(orc, cfg))
+    L, dth, th0 = 1800, 0.1, -90.0
+    assert th0 + (L - 1) * dth != -th0
+    u = 2 * 0.5 * np.sin(np.deg2rad(th0 + np.arange(L) * dth))
+    A = np.exp(-1j * np.pi * np.outer(np.arange(cfg.M), u))
+    Cm, _ = orc.projector("music", cfg.D, lam, V)
+    q = np.einsum("ml,mn,nl->l", A.conj(), Cm, A).real
+    f, _ = orc.spectrum("music", cfg.D, 0.5, lam, V, th0, dth, L)
+    assert np.max(np.abs(f - q)) <= 1e3 * EPS * np.sum(np.abs(Cm)) * cfg.M
