@@ -17,8 +17,8 @@ def _declared():
 
 @pytest.fixture(scope="module")
 def lib():
-    from paper_2007_14135_b200 import build
-    build.build()
+    import __graft_entry__
+    __graft_entry__.build()           # builds libdoa.so in a fresh checkout, then imports the package
     import paper_2007_14135_b200 as d
     return d
 
