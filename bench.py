@@ -324,10 +324,16 @@ def main():
     total_frames = B * ws
     value = total_frames / (ms_step / 1e3)
 
-    # roofline of the dominant kernel: the scan (S4-S6) inside doa_spectrum
+    # roofline of the dominant kernel: the scan (S4-S6) inside doa_spectrum.  On a symmetric grid
+    # (Q26) the scan evaluates each mirrored angle pair with one contraction, so the
+    # algorithmic work per angle is half that of the per-angle form.
+    mirrored = (not is_array and cfg.theta0 + float(L - 1) * cfg.dtheta == -cfg.theta0
+                and os.environ.get("DOA_SCAN_MIRROR", "1") != "0")
     spec_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in spec_ev)
     if is_array:                                   # K - 1 = M(M-1) fp64 FMAs per (frame, grid point)
         scan_flops = 2.0 * M * (M - 1) * L * B
+    elif mirrored:                                 # per mirrored pair: E and O (2(M-1) FMAs), E +- O (2 adds)
+        scan_flops = (2.0 * (M - 1) + 1.0) * L * B
     else:                                          # 2(M-1) fp64 FMAs per (frame, angle)
         scan_flops = 4.0 * (M - 1) * L * B
     pk = peaks_json()
@@ -344,6 +350,7 @@ def main():
                                   "(profiles/traffic.json); algorithmic operand bytes per launch: coef 16.8 MB",
                 "kernel": "doa_spectrum = coef_kernel + scan kernel (FP64 DMMA mma.sync m8n8k4); events "
                           "bracket both, so the scan's own fraction is higher",
+                "algorithmic_flops_per_point": scan_flops / (L * B), "mirrored_scan": mirrored,
                 "kernel_ms": spec_ms, "share_of_step": spec_ms * len(ALGS) / ms_step,
                 "peak_source": "148 SMs x 64 FP64 lanes x 2 flop x sm_max_mhz (guide unit counts; "
                                "measured DMMA 37.18 / DFMA 34.19 TFLOP/s in profiles/fp64_peaks_r01.txt)"}

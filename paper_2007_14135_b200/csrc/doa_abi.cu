@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -123,6 +124,16 @@ doa_status_t doa_plan_create(doa_plan_t* plan, int32_t M, double d_over_lambda, 
   std::memset(p, 0, sizeof *p);
   p->M = M; p->D = D; p->alg = alg; p->dl = d_over_lambda; p->theta0 = theta0_deg; p->dtheta = dtheta_deg;
   p->L = L; p->max_batch = max_batch;
+  // Q26: a grid whose last point (Q8 arithmetic) is exactly -theta0 is built from both ends and the
+  // scan evaluates mirrored angle pairs together.  DOA_SCAN_MIRROR=0 (A/B and tests only) keeps
+  // the symmetric grid but scans every angle separately.
+  {
+    volatile double end = (double)(L - 1) * dtheta_deg;   // rounded multiply, then rounded add (no FMA)
+    end = end + theta0_deg;
+    p->sym = (end == -theta0_deg) ? 1 : 0;
+    const char* ev = std::getenv("DOA_SCAN_MIRROR");
+    p->mirror = p->sym && !(ev && ev[0] == '0');
+  }
   // interior minima of a degree-(M-1) trig polynomial over ceil(2 d/lambda) periods, x2 margin, >= 32
   int cap = 2 * ((M - 1) * (int)std::ceil(2.0 * d_over_lambda) + 1);
   cap = (cap + 31) & ~31;

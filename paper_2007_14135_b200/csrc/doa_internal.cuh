@@ -12,17 +12,24 @@ constexpr int kMaxM = 64;
 constexpr int kMaxSweeps = 30;          // Q15
 constexpr double kFloor = 1e-300;       // Q12
 
-// Coefficient vector per frame, K = 4*S entries (S = ksteps(M) k-steps of 4, K >= 2M-1):
-//   coef[0]         = c_0                     (real; trace of C)
-//   coef[k]         = 2 Re c_k,  k = 1..M-1   (multiplies cos(k psi))
-//   coef[M-1+k]     = 2 Im c_k,  k = 1..M-1   (multiplies sin(k psi))
-//   coef[j]         = 0,         j >= 2M-1    (padding)
-// so that f(psi) = sum_j coef[j] T_j(psi) with T = (1, cos psi..cos (M-1)psi, sin psi..sin (M-1)psi, 0..)
-// and psi = pi u, u = 2 (d/lambda) sin(theta).  c_k = sum_p C[p][p+k].
+// Coefficient vector per frame, K = 4*S entries in two k-step-aligned halves, S = SE + SO k-steps of
+// 4 with SE = ceil(M/4) (even part) and SO = ceil((M-1)/4) (odd part); SE = (S+1)/2 for every M:
+//   coef[0]             = c_0                 (real; trace of C)
+//   coef[k]             = 2 Re c_k, k = 1..M-1 (multiplies cos(k psi))        j <  4 SE: even part
+//   coef[4 SE + k - 1]  = 2 Im c_k, k = 1..M-1 (multiplies sin(k psi))        j >= 4 SE: odd part
+//   every other j       = 0                    (padding)
+// so that f(psi) = E(psi) + O(psi), E = sum_{j<4SE} coef[j] T_j(psi) even in psi and
+// O = sum_{j>=4SE} coef[j] T_j(psi) odd in psi, with T = (1, cos psi..cos (M-1)psi, 0.., sin psi..
+// sin (M-1)psi, 0..) and psi = pi u, u = 2 (d/lambda) sin(theta).  c_k = sum_p C[p][p+k] (DESIGN.md
+// §5).  On a symmetric grid (Q26) the mirrored angle has psi -> -psi, so f = E - O there: one
+// contraction serves both angles of a mirrored pair.
 // Stored in the DMMA A-fragment order of 8-frame groups: element (b, j) lives at
 //   ((b/8)*S + j/4)*32 + (b%8)*4 + j%4
 // so one coalesced 8-byte load per k-step gives every lane its m8n8k4 A operand.
-__host__ __device__ constexpr int ksteps(int M) { return (2 * M + 3) / 4; }
+__host__ __device__ constexpr int ksteps_even(int M) { return (M + 3) / 4; }
+__host__ __device__ constexpr int ksteps(int M) { return (M + 3) / 4 + (M + 2) / 4; }
+__host__ __device__ constexpr int coef_cos(int k) { return k; }                          // k = 0..M-1
+__host__ __device__ constexpr int coef_sin(int M, int k) { return 4 * ksteps_even(M) + k - 1; }   // k = 1..M-1
 __host__ __device__ inline size_t coef_index(int64_t b, int j, int S) {
   return ((size_t)(b >> 3) * S + (j >> 2)) * 32 + (size_t)(b & 7) * 4 + (j & 3);
 }
@@ -35,6 +42,8 @@ struct doa_plan_s {
   int32_t geom;                   // 0: ULA (Toeplitz scan); 1: general array on an az x el grid
   double dl, theta0, dtheta;
   int64_t L, max_batch;
+  int32_t sym;                    // Q26: theta0 + (L-1) dtheta == -theta0 (grid built from both ends)
+  int32_t mirror;                 // scan evaluates mirrored angle pairs with one contraction (sym only)
   // general-array plans (geom == 1): grid az_i = az0 + i daz (i < naz), el_j = el0 + j del (j < nel),
   // flattened azimuth-major; element-pair position differences r_q - r_p (p < q) in wavelengths
   double az0, daz, el0, del;

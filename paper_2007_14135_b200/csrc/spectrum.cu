@@ -113,31 +113,41 @@ __global__ void __launch_bounds__(kCoefWarps * 32) coef_kernel(const double* __r
       for (int h2 = 0; h2 < H; ++h2) { const double2 v = part[h2 * (M <= 16 ? M : 32) + lane]; sr += v.x; si += v.y; }
       if (kk == 0) coef[coef_index(b, 0, S)] = sr;
       else {
-        coef[coef_index(b, kk, S)] = 2.0 * sr;
-        coef[coef_index(b, M - 1 + kk, S)] = 2.0 * si;
+        coef[coef_index(b, coef_cos(kk), S)] = 2.0 * sr;
+        coef[coef_index(b, coef_sin(M, kk), S)] = 2.0 * si;
       }
     }
     __syncwarp();
   }
-  for (int j = 2 * M - 1 + lane; j < 4 * S; j += 32) coef[coef_index(b, j, S)] = 0.0;   // K padding
+  const int JE = 4 * ksteps_even(M);
+  for (int j = lane; j < 4 * S; j += 32)                                                // K padding
+    if ((j >= M && j < JE) || j >= JE + M - 1) coef[coef_index(b, j, S)] = 0.0;
   if (lane == 0) {
     cnt[b] = 0;
     if (info) info[b] |= flag;
   }
 }
 
-// T_j(psi): j = 0 -> 1; 1..M-1 -> cos(j psi); M..2M-2 -> sin((j-M+1) psi); else 0.
-// psi = pi u; cospi/sinpi of the exact multiple j*u (one rounding) — no recurrence.
+// T_j(psi) in the split layout of doa_internal.cuh: j = 0 -> 1; 1..M-1 -> cos(j psi);
+// JE..JE+M-2 -> sin((j-JE+1) psi) with JE = 4 ceil(M/4); else 0.
+// psi = pi u; cospi/sinpi of the exact multiple j*u (one rounding) — no recurrence.  Both are
+// exactly even / odd in u, so T(-u) is T(u) with the odd half negated bit for bit.
 __device__ __forceinline__ double table_entry(int j, int M, double u) {
+  const int JE = 4 * ksteps_even(M);
   if (j == 0) return 1.0;
   if (j < M) return cospi((double)j * u);
-  if (j < 2 * M - 1) return sinpi((double)(j - M + 1) * u);
+  if (j >= JE && j < JE + M - 1) return sinpi((double)(j - JE + 1) * u);
   return 0.0;
 }
 
-__device__ __forceinline__ double grid_u(int64_t i, double theta0, double dtheta, double dl) {
-  const double th = __dadd_rn(__dmul_rn((double)i, dtheta), theta0);   // Q8: multiply then add
-  return 2.0 * dl * sinpi(th / 180.0);                                    // u = 2 (d/lambda) sin(theta)
+// Grid angle (Q8, Q26): theta_i = theta0 + i dtheta (rounded multiply, then rounded add); on a
+// symmetric grid the upper half i >= ceil(L/2) is built from the other end, -theta_{L-1-i}.
+// u = 2 (d/lambda) sin(theta) with sinpi, odd in theta, so mirrored angles give u exactly negated.
+__device__ __forceinline__ double grid_u(int64_t i, double theta0, double dtheta, double dl, int L, bool sym) {
+  double th;
+  if (sym && i >= (L + 1) / 2) th = -__dadd_rn(__dmul_rn((double)(L - 1 - i), dtheta), theta0);
+  else th = __dadd_rn(__dmul_rn((double)i, dtheta), theta0);
+  return 2.0 * dl * sinpi(th / 180.0);
 }
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
@@ -149,19 +159,24 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 // ---------------------------------------------------------------------------------------------
 // S4-S6: the scan on the FP64 tensor pipe (mma.sync m8n8k4 f64).
 //
-// Work tile = (angle column x, frame chunk y).  An angle column is NB = 2 consecutive angle blocks
-// of W = 8*NA grid angles (positions 0 and W-1 of a block are halo; blocks advance by W-2 so
-// every interior angle is decided by exactly one lane).  The steering table of a column is
-// generated once into shared memory in DMMA B-fragment order
+// Work tile = (angle column x, frame chunk y).  An angle column is NB consecutive angle blocks of
+// W = 8*NA grid angles (positions 0 and W-1 of a block are halo; blocks advance by W-2 so every
+// interior angle is decided by exactly one lane).  The steering table of a column is generated
+// once into shared memory in DMMA B-fragment order
 //     Ts[k][s][t][lane] = T_{4s + lane%4}(angle base_k + 8t + lane/4)
 // (fp64 sincospi, no recurrence) so every B-fragment load is one conflict-free 8-byte LDS.
 // The CTA's 8 warps stream disjoint 8-frame groups of the chunk (warp w: g0+w, g0+w+8, ...):
-// one coalesced A-fragment load per k-step (prefetched one group ahead, reused for both blocks),
+// one coalesced A-fragment load per k-step (prefetched one group ahead, reused for all blocks),
 // S x NA DMMAs per block (8 independent accumulator chains), then the fused epilogue:
 //   D fragment: lane holds frame lane/4, angles 8t + 2(lane%4) + {0,1}.
 //   floor (Q12) + peak test (Q9/Q10) in the INTEGER domain — for positive doubles the IEEE bits
 //   order like the values, so the FP64 pipe stays with the DMMAs; neighbours by shuffles inside
 //   each 4-lane frame row; rare atomic append to the frame's candidate list; optional fp32 P.
+// MIRROR (symmetric grids, Q26): the blocks cover only the lower half i <= H = ceil(L/2) (one
+// angle past the middle as the last neighbour); the even and odd k-steps accumulate separately,
+// E and O, and the tile yields f_i = E + O and f_{L-1-i} = E - O (psi_{L-1-i} = -psi_i exactly):
+// half the DMMAs and half the steering table per grid angle.  In the mirrored half the grid index
+// runs backwards through the tile, so the peak test's strict/non-strict sides swap.
 // Grid: blockIdx.x = angle column, blockIdx.y = frame chunk (~4 waves of resident CTAs).
 // (A persistent tile loop, a software-pipelined and a warp-specialised producer/consumer variant
 // were measured and were slower on c4; see profiles/README.md.)
@@ -169,152 +184,203 @@ constexpr int kCtaWarps = 8;
 constexpr long long kInfBits = 0x7FF0000000000000LL;        // bits of +inf
 constexpr long long kFloorBits = 0x01A56E1FC2F8F359LL;      // bits of 1e-300 (kFloor, Q12)
 
-// Shape by k-steps S = ceil((2M-1)/4) (M <= 64 -> S <= 32): 8 tiles of 8 angles per block; S <= 8
-// (M <= 16) keeps the A fragments of a group in registers with a one-group prefetch and uses two
-// blocks per column; larger S streams the A fragment of each k-step from L1/L2 and uses one block
-// (table: S x 8 x 32 doubles = up to 64 KB of smem).
-template <int S>
+// Shape by k-steps S (M <= 64 -> S <= 32): 8 tiles of 8 angles per block; S <= 8 (M <= 16) keeps
+// the A fragments of a group in registers with a one-group prefetch and uses two blocks per column
+// (one in the mirrored variant, whose two accumulator sets double the registers); larger S streams
+// the A fragment of each k-step from L1/L2 and uses one block (table: S x 8 x 32 doubles = up to
+// 64 KB of smem).
+template <int S, bool MIRROR>
 struct ScanShape {
   static constexpr int NA = 8;                               // 8-angle tiles per block
   static constexpr int W = 8 * NA;                           // angles per block (incl. 2 halo)
   static constexpr bool STREAM_A = S > 8;
-  static constexpr int NB = STREAM_A ? 1 : 2;                // blocks per column
+  static constexpr int NB = (STREAM_A || MIRROR) ? 1 : 2;    // blocks per column
+  static constexpr int SE = MIRROR ? (S + 1) / 2 : S;        // k-steps of the even part E
 };
 
-template <int S, bool WRITE_P>
+// Floor (Q12), neighbour exchange, peak test (Q9/Q10), candidate append and optional fp32 P for
+// one accumulator set.  REV: the set holds grid index L-1-i at tile index i (mirrored half).
+// Decided tile indices: interior positions 1..W-2 with i in [ilo, ihi]; P written for i in [0, whi].
+template <int NA, bool WRITE_P, bool REV>
+__device__ __forceinline__ void scan_epilogue(long long (&fi)[NA][2], int lane, int base, int ilo, int ihi, int whi, int L,
+                                              int b, bool frame_ok, int cap, int32_t* __restrict__ cnt,
+                                              int32_t* __restrict__ cidx, double* __restrict__ cf,
+                                              float* __restrict__ P) {
+  constexpr int W = 8 * NA;
+  const int q = lane & 3;
+  const int srcL = q > 0 ? lane - 1 : lane + 3;
+  const int srcR = q < 3 ? lane + 1 : lane - 3;
+  // Fast path: if every value of the warp's tile is a positive double above the floor and not NaN
+  // (checked on the high words, conservatively), the raw bits already are the floored values;
+  // otherwise the whole tile takes the explicit floor, which maps negative values, +-0 and NaNs to
+  // 1e-300 like the oracle's max(f, 1e-300) (Q12).
+  int hmin = 0x7FFFFFFF, hmax = (int)0x80000000;
+#pragma unroll
+  for (int t = 0; t < NA; ++t)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int hi = (int)(fi[t][e] >> 32);
+      hmin = min(hmin, hi);
+      hmax = max(hmax, hi);
+    }
+  if (__any_sync(0xffffffffu, hmin <= (int)(kFloorBits >> 32) || hmax >= (int)(kInfBits >> 32))) {
+#pragma unroll
+    for (int t = 0; t < NA; ++t)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        long long v = fi[t][e];
+        v = v > kInfBits ? kFloorBits : v;
+        fi[t][e] = v > kFloorBits ? v : kFloorBits;
+      }
+  }
+  // neighbours in tile order: left of (t,q,0) is (t,q-1,1) [q>0] or (t-1,3,1) [q=0];
+  //                           right of (t,q,1) is (t,q+1,0) [q<3] or (t+1,0,0) [q=3]
+  long long up[NA], dn[NA];
+#pragma unroll
+  for (int t = 0; t < NA; ++t) {
+    up[t] = __shfl_sync(0xffffffffu, fi[t][1], srcL);
+    dn[t] = __shfl_sync(0xffffffffu, fi[t][0], srcR);
+  }
+  // lane pair (v0, v1) with outer tile neighbours Lt, Rt.  Forward: c = v1 < v0;
+  // v0 is a minimum iff !c && v0 < Lt;  v1 iff c && v1 <= Rt   (Q10: f_i < f_{i-1}, f_i <= f_{i+1}).
+  // REV (grid index decreasing along the tile): c = v0 < v1; v0 iff c && v0 <= Lt; v1 iff !c && v1 < Rt.
+  unsigned hit = 0;
+#pragma unroll
+  for (int t = 0; t < NA; ++t) {
+    const long long fl0 = q > 0 ? up[t] : (t > 0 ? up[t - 1] : fi[t][0]);
+    const long long fr1 = q < 3 ? dn[t] : (t + 1 < NA ? dn[t + 1] : fi[t][1]);
+    if (!REV) {
+      const bool c = fi[t][1] < fi[t][0];
+      hit |= (unsigned)(!c && fi[t][0] < fl0) << (2 * t);
+      hit |= (unsigned)(c && fi[t][1] <= fr1) << (2 * t + 1);
+    } else {
+      const bool c = fi[t][0] < fi[t][1];
+      hit |= (unsigned)(c && fi[t][0] <= fl0) << (2 * t);
+      hit |= (unsigned)(!c && fi[t][1] < fr1) << (2 * t + 1);
+    }
+  }
+  if (!frame_ok) hit = 0;
+  while (hit) {                                            // local maxima of P (rare)
+    const int kk = __ffs(hit) - 1;
+    hit &= hit - 1;
+    const int t = kk >> 1, e = kk & 1;
+    const int pos = 8 * t + 2 * q + e, i = base + pos;
+    if (pos < 1 || pos > W - 2 || i < ilo || i > ihi) continue;   // halo / grid ends (Q9)
+    long long f = 0;
+#pragma unroll
+    for (int tt = 0; tt < NA; ++tt)
+      if (tt == t) f = e ? fi[tt][1] : fi[tt][0];
+    const int slot = atomicAdd(cnt + b, 1);
+    if (slot < cap) {
+      cidx[(size_t)b * cap + slot] = REV ? L - 1 - i : i;
+      cf[(size_t)b * cap + slot] = __longlong_as_double(f);
+    }
+  }
+  if (WRITE_P && frame_ok) {
+    float* Pb = P + (size_t)b * L;
+#pragma unroll
+    for (int t = 0; t < NA; ++t)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int pos = 8 * t + 2 * q + e, i = base + pos;
+        if (pos >= 1 && pos <= W - 2 && i >= 0 && i <= whi)
+          Pb[REV ? L - 1 - i : i] = to_p32(__longlong_as_double(fi[t][e]));
+      }
+  }
+}
+
+template <int S, bool WRITE_P, bool MIRROR>
 __global__ void __launch_bounds__(kCtaWarps * 32, 2) scan_cta_kernel(const double* __restrict__ coef, int64_t B, int M,
                                                                    int64_t per, double dl, double theta0, double dtheta, int L,
-                                                                   int cap, int32_t* __restrict__ cnt,
+                                                                   bool sym, int cap, int32_t* __restrict__ cnt,
                                                                    int32_t* __restrict__ cidx,
                                                                    double* __restrict__ cf, float* __restrict__ P) {
-  constexpr int NA = ScanShape<S>::NA, W = ScanShape<S>::W, NB = ScanShape<S>::NB;
-  constexpr bool STREAM_A = ScanShape<S>::STREAM_A;
+  using Shape = ScanShape<S, MIRROR>;
+  constexpr int NA = Shape::NA, W = Shape::W, NB = Shape::NB, SE = Shape::SE;
+  constexpr bool STREAM_A = Shape::STREAM_A;
   constexpr int SA = STREAM_A ? 1 : S;                           // register-held A fragments
   extern __shared__ double Ts[];                                 // [NB][S][NA][32]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int q = lane & 3, r = lane >> 2;
-  const int srcL = q > 0 ? lane - 1 : lane + 3;
-  const int srcR = q < 3 ? lane + 1 : lane - 3;
+  const int r = lane >> 2;
+  const int H = (L + 1) / 2;                                     // lower half [0, H) (MIRROR)
+  const int Lt = MIRROR ? H + 1 : L;                             // table-valid tile indices [0, Lt)
   const int64_t ngroups = (B + 7) / 8;
-  {
-    const int64_t y = blockIdx.y;
-    const int blk0 = (int)blockIdx.x * NB;
-    for (int e = threadIdx.x; e < NB * S * NA * 32; e += kCtaWarps * 32) {
-      const int ln = e & 31, t = (e >> 5) % NA, s = (e / (32 * NA)) % S, k = e / (32 * NA * S);
-      const int i = (blk0 + k) * (W - 2) - 1 + 8 * t + (ln >> 2);
-      const int j = 4 * s + (ln & 3);
-      double v = (j == 0) ? 1.0 : 0.0;
-      if (i >= 0 && i < L) v = table_entry(j, M, grid_u(i, theta0, dtheta, dl));
-      Ts[e] = v;
-    }
-    __syncthreads();
-    const int64_t g0 = y * per;
-    const int64_t g1 = (g0 + per < ngroups) ? g0 + per : ngroups;
-    double an[SA];
-    if (!STREAM_A && g0 + warp < g1) {
-      const double* cg = coef + ((size_t)(g0 + warp) * S) * 32 + lane;
+  const int64_t y = blockIdx.y;
+  const int blk0 = (int)blockIdx.x * NB;
+  for (int e = threadIdx.x; e < NB * S * NA * 32; e += kCtaWarps * 32) {
+    const int ln = e & 31, t = (e >> 5) % NA, s = (e / (32 * NA)) % S, k = e / (32 * NA * S);
+    const int i = (blk0 + k) * (W - 2) - 1 + 8 * t + (ln >> 2);
+    const int j = 4 * s + (ln & 3);
+    double v = (j == 0) ? 1.0 : 0.0;
+    if (i >= 0 && i < Lt) v = table_entry(j, M, grid_u(i, theta0, dtheta, dl, L, sym));
+    Ts[e] = v;
+  }
+  __syncthreads();
+  const int64_t g0 = y * per;
+  const int64_t g1 = (g0 + per < ngroups) ? g0 + per : ngroups;
+  double an[SA];
+  if (!STREAM_A && g0 + warp < g1) {
+    const double* cg = coef + ((size_t)(g0 + warp) * S) * 32 + lane;
 #pragma unroll
-      for (int s = 0; s < SA; ++s) an[s] = __ldg(cg + s * 32);
-    }
-    for (int64_t g = g0 + warp; g < g1; g += kCtaWarps) {
-      const double* cgc = coef + ((size_t)g * S) * 32 + lane;   // this group's A fragments
-      double a[SA];
-      if (!STREAM_A) {
+    for (int s = 0; s < SA; ++s) an[s] = __ldg(cg + s * 32);
+  }
+  for (int64_t g = g0 + warp; g < g1; g += kCtaWarps) {
+    const double* cgc = coef + ((size_t)g * S) * 32 + lane;   // this group's A fragments
+    double a[SA];
+    if (!STREAM_A) {
 #pragma unroll
-        for (int s = 0; s < SA; ++s) a[s] = an[s];
-        if (g + kCtaWarps < g1) {                                // prefetch the next group's operands
-          const double* cg = coef + ((size_t)(g + kCtaWarps) * S) * 32 + lane;
+      for (int s = 0; s < SA; ++s) a[s] = an[s];
+      if (g + kCtaWarps < g1) {                                // prefetch the next group's operands
+        const double* cg = coef + ((size_t)(g + kCtaWarps) * S) * 32 + lane;
 #pragma unroll
-          for (int s = 0; s < SA; ++s) an[s] = __ldg(cg + s * 32);
-        }
+        for (int s = 0; s < SA; ++s) an[s] = __ldg(cg + s * 32);
       }
-      const int b = (int)(g * 8) + r;
-      const bool frame_ok = b < B;
+    }
+    const int b = (int)(g * 8) + r;
+    const bool frame_ok = b < B;
 #pragma unroll 1
-      for (int k = 0; k < NB; ++k) {
-        const int base = (blk0 + k) * (W - 2) - 1;
-        if (base + 1 >= L) break;                                // warp-uniform
-        const double* Tk = Ts + (size_t)k * S * NA * 32 + lane;
-        double acc[NA][2];
+    for (int k = 0; k < NB; ++k) {
+      const int base = (blk0 + k) * (W - 2) - 1;
+      if (base + 1 >= (MIRROR ? H : L)) break;                 // warp-uniform
+      const double* Tk = Ts + (size_t)k * S * NA * 32 + lane;
+      double acc[NA][2], aco[MIRROR ? NA : 1][2];
 #pragma unroll
-        for (int t = 0; t < NA; ++t) { acc[t][0] = 0.0; acc[t][1] = 0.0; }
+      for (int t = 0; t < NA; ++t) { acc[t][0] = 0.0; acc[t][1] = 0.0; }
+      if (MIRROR) {
 #pragma unroll
-        for (int s = 0; s < S; ++s) {
-          const double av = STREAM_A ? __ldg(cgc + s * 32) : a[STREAM_A ? 0 : s];
+        for (int t = 0; t < (MIRROR ? NA : 1); ++t) { aco[t][0] = 0.0; aco[t][1] = 0.0; }
+      }
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const double av = STREAM_A ? __ldg(cgc + s * 32) : a[STREAM_A ? 0 : s];
+        if (!MIRROR || s < SE) {
 #pragma unroll
           for (int t = 0; t < NA; ++t) dmma_884(acc[t][0], acc[t][1], av, Tk[(s * NA + t) * 32]);
+        } else {
+#pragma unroll
+          for (int t = 0; t < (MIRROR ? NA : 1); ++t) dmma_884(aco[t][0], aco[t][1], av, Tk[(s * NA + t) * 32]);
         }
-        // Fast path: if every value of the warp's tile is a positive double above the floor and
-        // not NaN (checked on the high words, conservatively), the raw bits already are the
-        // floored values; otherwise the whole tile takes the explicit floor, which maps negative
-        // values, +-0 and NaNs to 1e-300 like the oracle's max(f, 1e-300) (Q12).
+      }
+      if (!MIRROR) {
         long long fi[NA][2];
-        int hmin = 0x7FFFFFFF, hmax = (int)0x80000000;
+#pragma unroll
+        for (int t = 0; t < NA; ++t) {
+          fi[t][0] = __double_as_longlong(acc[t][0]);
+          fi[t][1] = __double_as_longlong(acc[t][1]);
+        }
+        scan_epilogue<NA, WRITE_P, false>(fi, lane, base, 1, L - 2, L - 1, L, b, frame_ok, cap, cnt, cidx, cf, P);
+      } else {
+        long long fl[NA][2], fh[NA][2];
 #pragma unroll
         for (int t = 0; t < NA; ++t)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            fi[t][e] = __double_as_longlong(acc[t][e]);
-            const int hi = (int)(fi[t][e] >> 32);
-            hmin = min(hmin, hi);
-            hmax = max(hmax, hi);
+            const double ev = acc[t][e], od = aco[MIRROR ? t : 0][e];
+            fl[t][e] = __double_as_longlong(ev + od);           // f_i          = E + O
+            fh[t][e] = __double_as_longlong(ev - od);           // f_{L-1-i}    = E - O
           }
-        if (__any_sync(0xffffffffu, hmin <= (int)(kFloorBits >> 32) || hmax >= (int)(kInfBits >> 32))) {
-#pragma unroll
-          for (int t = 0; t < NA; ++t)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              long long v = fi[t][e];
-              v = v > kInfBits ? kFloorBits : v;
-              fi[t][e] = v > kFloorBits ? v : kFloorBits;
-            }
-        }
-        // neighbours: left of (t,q,0) is (t,q-1,1) [q>0] or (t-1,3,1) [q=0];
-        //             right of (t,q,1) is (t,q+1,0) [q<3] or (t+1,0,0) [q=3]
-        long long up[NA], dn[NA];
-#pragma unroll
-        for (int t = 0; t < NA; ++t) {
-          up[t] = __shfl_sync(0xffffffffu, fi[t][1], srcL);
-          dn[t] = __shfl_sync(0xffffffffu, fi[t][0], srcR);
-        }
-        // lane pair (v0, v1) with outer neighbours L, R: c = v1 < v0;
-        // v0 is a minimum iff !c && v0 < L;  v1 is a minimum iff c && v1 <= R   (Q10)
-        unsigned hit = 0;
-#pragma unroll
-        for (int t = 0; t < NA; ++t) {
-          const long long fl0 = q > 0 ? up[t] : (t > 0 ? up[t - 1] : fi[t][0]);
-          const long long fr1 = q < 3 ? dn[t] : (t + 1 < NA ? dn[t + 1] : fi[t][1]);
-          const bool c = fi[t][1] < fi[t][0];
-          hit |= (unsigned)(!c && fi[t][0] < fl0) << (2 * t);
-          hit |= (unsigned)(c && fi[t][1] <= fr1) << (2 * t + 1);
-        }
-        if (!frame_ok) hit = 0;
-        while (hit) {                                            // local maxima of P (rare)
-          const int kk = __ffs(hit) - 1;
-          hit &= hit - 1;
-          const int t = kk >> 1, e = kk & 1;
-          const int pos = 8 * t + 2 * q + e, i = base + pos;
-          if (pos < 1 || pos > W - 2 || i < 1 || i > L - 2) continue;   // halo / grid ends (Q9)
-          long long f = 0;
-#pragma unroll
-          for (int tt = 0; tt < NA; ++tt)
-            if (tt == t) f = e ? fi[tt][1] : fi[tt][0];
-          const int slot = atomicAdd(cnt + b, 1);
-          if (slot < cap) {
-            cidx[(size_t)b * cap + slot] = i;
-            cf[(size_t)b * cap + slot] = __longlong_as_double(f);
-          }
-        }
-        if (WRITE_P && frame_ok) {
-          float* Pb = P + (size_t)b * L;
-#pragma unroll
-          for (int t = 0; t < NA; ++t)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int pos = 8 * t + 2 * q + e, i = base + pos;
-              if (pos >= 1 && pos <= W - 2 && i >= 0 && i < L) Pb[i] = to_p32(__longlong_as_double(fi[t][e]));
-            }
-        }
+        scan_epilogue<NA, WRITE_P, false>(fl, lane, base, 1, H - 1, H - 1, L, b, frame_ok, cap, cnt, cidx, cf, P);
+        scan_epilogue<NA, WRITE_P, true>(fh, lane, base, 1, L - 1 - H, L - 1 - H, L, b, frame_ok, cap, cnt, cidx, cf, P);
       }
     }
   }
@@ -331,18 +397,20 @@ int sm_count() {
   return n;
 }
 
-template <int S>
+template <int S, bool MIRROR>
 cudaError_t launch_scan_cta(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
-  constexpr int NA = ScanShape<S>::NA, W = ScanShape<S>::W, NB = ScanShape<S>::NB;
+  using Shape = ScanShape<S, MIRROR>;
+  constexpr int NA = Shape::NA, W = Shape::W, NB = Shape::NB;
   const size_t smem = (size_t)NB * S * NA * 32 * sizeof(double);
   static int occ = 0;
   if (!occ) {
-    cudaFuncSetAttribute(scan_cta_kernel<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(scan_cta_kernel<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_cta_kernel<S, false>, kCtaWarps * 32, smem);
+    cudaFuncSetAttribute(scan_cta_kernel<S, false, MIRROR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(scan_cta_kernel<S, true, MIRROR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_cta_kernel<S, false, MIRROR>, kCtaWarps * 32, smem);
     if (occ < 1) occ = 1;
   }
-  const int64_t nwb = (p->L + (W - 2) - 1) / (W - 2);           // angle blocks owning [0, L)
+  const int64_t span = MIRROR ? (p->L + 1) / 2 : p->L;          // tile indices the blocks own
+  const int64_t nwb = (span + (W - 2) - 1) / (W - 2);            // angle blocks owning [0, span)
   const int64_t gx = (nwb + NB - 1) / NB;                        // angle columns
   const int64_t ngroups = (B + 7) / 8;
   const int64_t slots = (int64_t)sm_count() * occ;
@@ -352,14 +420,14 @@ cudaError_t launch_scan_cta(const doa_plan_s* p, int64_t B, float* P, cudaStream
   if (per > ngroups) per = ngroups;
   const int64_t gy = (ngroups + per - 1) / per;
   const dim3 grid((unsigned)gx, (unsigned)gy);
+  const bool sym = p->sym != 0;
   count_launch();
   if (P)
-    scan_cta_kernel<S, true><<<grid, kCtaWarps * 32, smem, s>>>(p->coef, B, p->M, per, p->dl, p->theta0, p->dtheta,
-                                                               (int)p->L, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
+    scan_cta_kernel<S, true, MIRROR><<<grid, kCtaWarps * 32, smem, s>>>(
+        p->coef, B, p->M, per, p->dl, p->theta0, p->dtheta, (int)p->L, sym, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
   else
-    scan_cta_kernel<S, false><<<grid, kCtaWarps * 32, smem, s>>>(p->coef, B, p->M, per, p->dl, p->theta0,
-                                                                p->dtheta, (int)p->L, p->cap, p->cnt, p->cand_idx,
-                                                                p->cand_f, P);
+    scan_cta_kernel<S, false, MIRROR><<<grid, kCtaWarps * 32, smem, s>>>(
+        p->coef, B, p->M, per, p->dl, p->theta0, p->dtheta, (int)p->L, sym, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
   return cudaGetLastError();
 }
 
@@ -424,7 +492,8 @@ cudaError_t launch_coef(const doa_plan_s* p, const double* lam, const double* V,
 
 cudaError_t launch_scan(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
   switch (ksteps(p->M)) {
-#define DOA_SCAN_CASE(k) case k: return launch_scan_cta<k>(p, B, P, s);
+#define DOA_SCAN_CASE(k) \
+  case k: return p->mirror ? launch_scan_cta<k, true>(p, B, P, s) : launch_scan_cta<k, false>(p, B, P, s);
     DOA_SCAN_CASE(1) DOA_SCAN_CASE(2) DOA_SCAN_CASE(3) DOA_SCAN_CASE(4) DOA_SCAN_CASE(5) DOA_SCAN_CASE(6)
     DOA_SCAN_CASE(7) DOA_SCAN_CASE(8) DOA_SCAN_CASE(9) DOA_SCAN_CASE(10) DOA_SCAN_CASE(11) DOA_SCAN_CASE(12)
     DOA_SCAN_CASE(13) DOA_SCAN_CASE(14) DOA_SCAN_CASE(15) DOA_SCAN_CASE(16) DOA_SCAN_CASE(17) DOA_SCAN_CASE(18)

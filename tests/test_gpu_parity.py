@@ -229,6 +229,61 @@ def test_geometry_and_grid_variants(doa, M, D, dl, theta0, dtheta, L):
             _check_frame(o, idx[b], P[b], alg, M, D, f"M={M} dl={dl} b={b}", check_db=L > 3)
 
 
+def _symmetric(theta0, dtheta, L):
+    """Q26 test: the grid's last point in Q8 arithmetic is exactly -theta0."""
+    return theta0 + float(L - 1) * dtheta == -theta0
+
+
+@pytest.mark.parametrize("mirror", ["1", "0"])
+@pytest.mark.parametrize("M,D,theta0,dtheta,L", [
+    (16, 4, -90.0, 60.0, 4), (16, 4, -90.0, 45.0, 5), (8, 2, -90.0, 36.0, 6), (8, 2, -90.0, 30.0, 7),
+    (16, 3, -62.0, 1.0, 125), (16, 3, -62.5, 1.0, 126), (16, 3, -63.0, 1.0, 127), (16, 3, -61.5, 1.0, 124),
+    (5, 2, -60.0, 0.5, 241), (13, 3, -90.0, 0.25, 721), (64, 8, -90.0, 0.125, 1441), (33, 5, -90.0, 0.5, 361),
+    (16, 4, -90.0, 0.0625, 2881)])
+def test_symmetric_grid_mirrored_scan(doa, monkeypatch, mirror, M, D, theta0, dtheta, L):
+    """Q26 grids through the mirrored scan (one contraction per mirrored angle pair) and, with
+    DOA_SCAN_MIRROR=0, through the per-angle scan on the same symmetric grid: both equal the oracle
+    (peaks exactly or certified ties, P within 1e-3 dB).  Odd and even L, L around the 62-angle block
+    boundaries (H = 62, 63, 64), M with odd/even k-step halves, M = 64 (streamed A fragments)."""
+    assert _symmetric(theta0, dtheta, L)
+    monkeypatch.setenv("DOA_SCAN_MIRROR", mirror)
+    cfg = get_config("c2").with_(M=M, D=D, N=300, sources=tuple(np.linspace(-40, 40, D)),
+                                 theta0=theta0, dtheta=dtheta)
+    B = 11
+    X = generate(cfg, frames=range(B))
+    for alg in ALGS:
+        plan = doa.Plan(M, D, alg, dtheta, L=L, theta0=theta0, max_batch=B)
+        idx, val, npk, info, P = plan.run(torch.from_numpy(X).cuda(), want_P=True)
+        idx, P = idx.cpu().numpy(), P.cpu().numpy()
+        for b in range(B):
+            o = _oracle_frame(X[b], alg, D, 0.5, theta0, dtheta, L)
+            _check_frame(o, idx[b], P[b], alg, M, D, f"mirror={mirror} L={L} b={b}", check_db=L > 5)
+        plan.close()
+
+
+def test_mirrored_and_plain_scan_agree(doa, monkeypatch):
+    """The two scan variants on the c4 grid (symmetric, L = 18001) differ only by the rounding of
+    E + O vs the direct sum: spectra agree to 1e-9 relative and every peak index agrees or the
+    oracle certifies the tie."""
+    cfg = get_config("c4")
+    assert _symmetric(cfg.theta0, cfg.dtheta, cfg.L)
+    B = 512
+    X = generate(cfg, frames=range(B))
+    Xd = torch.from_numpy(X).cuda()
+    out = {}
+    for m in ("1", "0"):
+        monkeypatch.setenv("DOA_SCAN_MIRROR", m)
+        plan = doa.Plan(cfg.M, cfg.D, "mn", cfg.dtheta, max_batch=B)
+        out[m] = [t.cpu().numpy() for t in plan.run(Xd, want_P=True)]
+        plan.close()
+    Pm, Pp = out["1"][4].astype(np.float64), out["0"][4].astype(np.float64)
+    assert np.max(np.abs(Pm - Pp) / Pp) <= 1e-6           # fp32 output rounding
+    for b in np.nonzero(np.any(out["1"][0] != out["0"][0], axis=1))[0]:
+        o = _oracle_frame(X[b], "mn", cfg.D, 0.5, cfg.theta0, cfg.dtheta, cfg.L)
+        for g in ("1", "0"):
+            _check_frame(o, out[g][0][b], None, "mn", cfg.M, cfg.D, f"frame {b} mirror={g}")
+
+
 def test_determinism_and_batch_invariance(doa):
     cfg = get_config("c4")
     X = torch.from_numpy(generate(cfg, frames=range(300))).cuda()
