@@ -31,19 +31,42 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Compile every csrc/*.cu to an object in parallel (nvcc -c), then link libdoa.so."""
     if out == LIB and not force and not stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     tmp = out + ".tmp"
-    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-o", tmp, *sources()]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    objdir = tmp + ".objs"
+    os.makedirs(objdir, exist_ok=True)
+    comp = [f for f in FLAGS if f not in ("-shared", "-cudart", "static")]
+    defs = [f"-D{d}" for d in defines]
+
+    def one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        r = subprocess.run([NVCC, *ARCH, *comp, *defs, "-c", "-o", obj, src], capture_output=True, text=True)
+        return src, obj, r
+
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        res = list(ex.map(one, sources()))
+    report = "".join(r.stdout + r.stderr for _, _, r in res)
+    bad = [src for src, _, r in res if r.returncode != 0]
+    if bad:
+        sys.stderr.write(report)
+        raise RuntimeError(f"nvcc failed building libdoa.so: {bad}")
+    r = subprocess.run([NVCC, *ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fPIC", "-o", tmp,
+                        *[o for _, o, _ in res]], capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libdoa.so")
-    with open(os.path.join(HERE, "ptxas_report.txt"), "w") as fh:
-        fh.write(r.stderr)
+        raise RuntimeError("nvcc failed linking libdoa.so")
+    if out == LIB:
+        with open(os.path.join(HERE, "ptxas_report.txt"), "w") as fh:
+            fh.write(report)
     if verbose:
-        sys.stderr.write(r.stderr)
+        sys.stderr.write(report)
     os.replace(tmp, out)
+    for _, o, _ in res:
+        os.remove(o)
+    os.rmdir(objdir)
     return out
 
 

@@ -150,6 +150,17 @@ __device__ __forceinline__ double grid_u(int64_t i, double theta0, double dtheta
   return 2.0 * dl * sinpi(th / 180.0);
 }
 
+// Named barriers over the CTA's 256 threads (id 0 is __syncthreads): bar_sync waits until the
+// 128 threads of the other warp group have arrived; bar_arrive signals without waiting.
+__device__ __forceinline__ void bar_sync(int id) {
+  if (id == 1) asm volatile("bar.sync 1, 256;\n" ::: "memory");
+  else asm volatile("bar.sync 2, 256;\n" ::: "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id) {
+  if (id == 1) asm volatile("bar.arrive 1, 256;\n" ::: "memory");
+  else asm volatile("bar.arrive 2, 256;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
@@ -168,10 +179,11 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 // The CTA's 8 warps stream disjoint 8-frame groups of the chunk (warp w: g0+w, g0+w+8, ...):
 // one coalesced A-fragment load per k-step (prefetched one group ahead, reused for all blocks),
 // S x NA DMMAs per block (8 independent accumulator chains), then the fused epilogue:
-//   D fragment: lane holds frame lane/4, angles 8t + 2(lane%4) + {0,1}.
+//   D fragment: lane holds frame lane/4, block positions 16(lane%4) + 0..15.
 //   floor (Q12) + peak test (Q9/Q10) in the INTEGER domain — for positive doubles the IEEE bits
-//   order like the values, so the FP64 pipe stays with the DMMAs; neighbours by shuffles inside
-//   each 4-lane frame row; rare atomic append to the frame's candidate list; optional fp32 P.
+//   order like the values, so the FP64 pipe stays with the DMMAs; 17 compares per 16 angles in
+//   registers, two shuffles for the run ends; rare atomic append to the frame's candidate list;
+//   optional fp32 P.
 // MIRROR (symmetric grids, Q26): the blocks cover only the lower half i <= H = ceil(L/2) (one
 // angle past the middle as the last neighbour); the even and odd k-steps accumulate separately,
 // E and O, and the tile yields f_i = E + O and f_{L-1-i} = E - O (psi_{L-1-i} = -psi_i exactly):
@@ -181,6 +193,22 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 // (A persistent tile loop, a software-pipelined and a warp-specialised producer/consumer variant
 // were measured and were slower on c4; see profiles/README.md.)
 constexpr int kCtaWarps = 8;
+// Tuning knobs (compile-time; tools/scan_variants.sh builds A/B libraries with -D overrides).
+#ifndef DOA_SCAN_NA
+#define DOA_SCAN_NA 8        // 8-angle tiles per block (a lane owns 2*NA consecutive angles)
+#endif
+#ifndef DOA_SCAN_MNB
+#define DOA_SCAN_MNB 1       // blocks per column in the mirrored scan
+#endif
+#ifndef DOA_SCAN_MINB
+#define DOA_SCAN_MINB 2      // __launch_bounds__ min blocks per SM
+#endif
+#ifndef DOA_SCAN_PP
+#define DOA_SCAN_PP 1        // ping-pong the DMMA pipe between the two warp groups of a CTA
+#endif
+#ifndef DOA_SCAN_PF
+#define DOA_SCAN_PF 1        // prefetch the next group's A fragments into registers
+#endif
 constexpr long long kInfBits = 0x7FF0000000000000LL;        // bits of +inf
 constexpr long long kFloorBits = 0x01A56E1FC2F8F359LL;      // bits of 1e-300 (kFloor, Q12)
 
@@ -191,85 +219,77 @@ constexpr long long kFloorBits = 0x01A56E1FC2F8F359LL;      // bits of 1e-300 (k
 // 64 KB of smem).
 template <int S, bool MIRROR>
 struct ScanShape {
-  static constexpr int NA = 8;                               // 8-angle tiles per block
+  static constexpr int NA = DOA_SCAN_NA;                     // 8-angle tiles per block
   static constexpr int W = 8 * NA;                           // angles per block (incl. 2 halo)
   static constexpr bool STREAM_A = S > 8;
-  static constexpr int NB = (STREAM_A || MIRROR) ? 1 : 2;    // blocks per column
+  static constexpr int NB = STREAM_A ? 1 : (MIRROR ? DOA_SCAN_MNB : 2);   // blocks per column
   static constexpr int SE = MIRROR ? (S + 1) / 2 : S;        // k-steps of the even part E
 };
 
+// Angle position inside a block of column n of 8-angle tile t: the D fragment gives lane (r, q)
+// columns n = 2q + e of every tile, so with this permutation of the table's columns lane q holds
+// the 16 CONSECUTIVE angles 16q + (2t + e) of its frame — the peak test runs in registers and only
+// the two run ends cross lanes.
+template <int NA>
+__host__ __device__ constexpr int tile_pos(int t, int n) { return 2 * NA * (n >> 1) + 2 * t + (n & 1); }
+
 // Floor (Q12), neighbour exchange, peak test (Q9/Q10), candidate append and optional fp32 P for
-// one accumulator set.  REV: the set holds grid index L-1-i at tile index i (mirrored half).
+// one accumulator set; v[j] (j = 2t + e) is the lane's angle at block position 16q + j.
+// REV: the set holds grid index L-1-i at tile index i (mirrored half).
 // Decided tile indices: interior positions 1..W-2 with i in [ilo, ihi]; P written for i in [0, whi].
 template <int NA, bool WRITE_P, bool REV>
-__device__ __forceinline__ void scan_epilogue(long long (&fi)[NA][2], int lane, int base, int ilo, int ihi, int whi, int L,
-                                              int b, bool frame_ok, int cap, int32_t* __restrict__ cnt,
+__device__ __forceinline__ void scan_epilogue(long long (&v)[2 * NA], int lane, int base, int ilo, int ihi, int whi,
+                                              int L, int b, bool frame_ok, int cap, int32_t* __restrict__ cnt,
                                               int32_t* __restrict__ cidx, double* __restrict__ cf,
                                               float* __restrict__ P) {
-  constexpr int W = 8 * NA;
+  constexpr int W = 8 * NA, R = 2 * NA;
   const int q = lane & 3;
-  const int srcL = q > 0 ? lane - 1 : lane + 3;
-  const int srcR = q < 3 ? lane + 1 : lane - 3;
   // Fast path: if every value of the warp's tile is a positive double above the floor and not NaN
   // (checked on the high words, conservatively), the raw bits already are the floored values;
   // otherwise the whole tile takes the explicit floor, which maps negative values, +-0 and NaNs to
-  // 1e-300 like the oracle's max(f, 1e-300) (Q12).
+  // 1e-300 like the oracle's max(f, 1e-300) (Q12).  For positive doubles the IEEE bits order like
+  // the values, so the whole test runs in the integer domain and the FP64 pipe stays with the DMMAs.
   int hmin = 0x7FFFFFFF, hmax = (int)0x80000000;
 #pragma unroll
-  for (int t = 0; t < NA; ++t)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int hi = (int)(fi[t][e] >> 32);
-      hmin = min(hmin, hi);
-      hmax = max(hmax, hi);
-    }
+  for (int j = 0; j < R; ++j) {
+    const int hi = (int)(v[j] >> 32);
+    hmin = min(hmin, hi);
+    hmax = max(hmax, hi);
+  }
   if (__any_sync(0xffffffffu, hmin <= (int)(kFloorBits >> 32) || hmax >= (int)(kInfBits >> 32))) {
 #pragma unroll
-    for (int t = 0; t < NA; ++t)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        long long v = fi[t][e];
-        v = v > kInfBits ? kFloorBits : v;
-        fi[t][e] = v > kFloorBits ? v : kFloorBits;
-      }
-  }
-  // neighbours in tile order: left of (t,q,0) is (t,q-1,1) [q>0] or (t-1,3,1) [q=0];
-  //                           right of (t,q,1) is (t,q+1,0) [q<3] or (t+1,0,0) [q=3]
-  long long up[NA], dn[NA];
-#pragma unroll
-  for (int t = 0; t < NA; ++t) {
-    up[t] = __shfl_sync(0xffffffffu, fi[t][1], srcL);
-    dn[t] = __shfl_sync(0xffffffffu, fi[t][0], srcR);
-  }
-  // lane pair (v0, v1) with outer tile neighbours Lt, Rt.  Forward: c = v1 < v0;
-  // v0 is a minimum iff !c && v0 < Lt;  v1 iff c && v1 <= Rt   (Q10: f_i < f_{i-1}, f_i <= f_{i+1}).
-  // REV (grid index decreasing along the tile): c = v0 < v1; v0 iff c && v0 <= Lt; v1 iff !c && v1 < Rt.
-  unsigned hit = 0;
-#pragma unroll
-  for (int t = 0; t < NA; ++t) {
-    const long long fl0 = q > 0 ? up[t] : (t > 0 ? up[t - 1] : fi[t][0]);
-    const long long fr1 = q < 3 ? dn[t] : (t + 1 < NA ? dn[t + 1] : fi[t][1]);
-    if (!REV) {
-      const bool c = fi[t][1] < fi[t][0];
-      hit |= (unsigned)(!c && fi[t][0] < fl0) << (2 * t);
-      hit |= (unsigned)(c && fi[t][1] <= fr1) << (2 * t + 1);
-    } else {
-      const bool c = fi[t][0] < fi[t][1];
-      hit |= (unsigned)(c && fi[t][0] <= fl0) << (2 * t);
-      hit |= (unsigned)(!c && fi[t][1] < fr1) << (2 * t + 1);
+    for (int j = 0; j < R; ++j) {
+      long long x = v[j];
+      x = x > kInfBits ? kFloorBits : x;
+      v[j] = x > kFloorBits ? x : kFloorBits;
     }
   }
+  // run ends: left of v[0] is lane q-1's v[R-1], right of v[R-1] is lane q+1's v[0]; positions 0
+  // and W-1 of the block are halo and never decided, so q = 0 / q = 3 take any value.
+  const long long vl = __shfl_sync(0xffffffffu, v[R - 1], q > 0 ? lane - 1 : lane);
+  const long long vr = __shfl_sync(0xffffffffu, v[0], q < 3 ? lane + 1 : lane);
+  // Forward (Q10: f_i < f_{i-1} and f_i <= f_{i+1}): with d_j = v_j < v_{j-1}, j is a minimum iff
+  // d_j && !d_{j+1}.  REV (grid index decreasing along the run): g_j = v_{j-1} < v_j, j is a
+  // minimum iff g_{j+1} && !g_j.
+  unsigned m = 0;
+#pragma unroll
+  for (int j = 0; j <= R; ++j) {
+    const long long cur = j < R ? v[j] : vr;
+    const long long prv = j > 0 ? v[j - 1] : vl;
+    m |= (unsigned)(REV ? (prv < cur) : (cur < prv)) << j;
+  }
+  unsigned hit = REV ? ((m >> 1) & ~m) : (m & ~(m >> 1));
+  hit &= (1u << R) - 1;
   if (!frame_ok) hit = 0;
   while (hit) {                                            // local maxima of P (rare)
-    const int kk = __ffs(hit) - 1;
+    const int j = __ffs(hit) - 1;
     hit &= hit - 1;
-    const int t = kk >> 1, e = kk & 1;
-    const int pos = 8 * t + 2 * q + e, i = base + pos;
+    const int pos = R * q + j, i = base + pos;
     if (pos < 1 || pos > W - 2 || i < ilo || i > ihi) continue;   // halo / grid ends (Q9)
     long long f = 0;
 #pragma unroll
-    for (int tt = 0; tt < NA; ++tt)
-      if (tt == t) f = e ? fi[tt][1] : fi[tt][0];
+    for (int jj = 0; jj < R; ++jj)
+      if (jj == j) f = v[jj];
     const int slot = atomicAdd(cnt + b, 1);
     if (slot < cap) {
       cidx[(size_t)b * cap + slot] = REV ? L - 1 - i : i;
@@ -279,18 +299,15 @@ __device__ __forceinline__ void scan_epilogue(long long (&fi)[NA][2], int lane, 
   if (WRITE_P && frame_ok) {
     float* Pb = P + (size_t)b * L;
 #pragma unroll
-    for (int t = 0; t < NA; ++t)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int pos = 8 * t + 2 * q + e, i = base + pos;
-        if (pos >= 1 && pos <= W - 2 && i >= 0 && i <= whi)
-          Pb[REV ? L - 1 - i : i] = to_p32(__longlong_as_double(fi[t][e]));
-      }
+    for (int j = 0; j < R; ++j) {
+      const int pos = R * q + j, i = base + pos;
+      if (pos >= 1 && pos <= W - 2 && i >= 0 && i <= whi) Pb[REV ? L - 1 - i : i] = to_p32(__longlong_as_double(v[j]));
+    }
   }
 }
 
 template <int S, bool WRITE_P, bool MIRROR>
-__global__ void __launch_bounds__(kCtaWarps * 32, 2) scan_cta_kernel(const double* __restrict__ coef, int64_t B, int M,
+__global__ void __launch_bounds__(kCtaWarps * 32, DOA_SCAN_MINB) scan_cta_kernel(const double* __restrict__ coef, int64_t B, int M,
                                                                    int64_t per, double dl, double theta0, double dtheta, int L,
                                                                    bool sym, int cap, int32_t* __restrict__ cnt,
                                                                    int32_t* __restrict__ cidx,
@@ -309,7 +326,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, 2) scan_cta_kernel(const doubl
   const int blk0 = (int)blockIdx.x * NB;
   for (int e = threadIdx.x; e < NB * S * NA * 32; e += kCtaWarps * 32) {
     const int ln = e & 31, t = (e >> 5) % NA, s = (e / (32 * NA)) % S, k = e / (32 * NA * S);
-    const int i = (blk0 + k) * (W - 2) - 1 + 8 * t + (ln >> 2);
+    const int i = (blk0 + k) * (W - 2) - 1 + tile_pos<NA>(t, ln >> 2);
     const int j = 4 * s + (ln & 3);
     double v = (j == 0) ? 1.0 : 0.0;
     if (i >= 0 && i < Lt) v = table_entry(j, M, grid_u(i, theta0, dtheta, dl, L, sym));
@@ -319,29 +336,39 @@ __global__ void __launch_bounds__(kCtaWarps * 32, 2) scan_cta_kernel(const doubl
   const int64_t g0 = y * per;
   const int64_t g1 = (g0 + per < ngroups) ? g0 + per : ngroups;
   double an[SA];
-  if (!STREAM_A && g0 + warp < g1) {
+  if (!STREAM_A && DOA_SCAN_PF && g0 + warp < g1) {
     const double* cg = coef + ((size_t)(g0 + warp) * S) * 32 + lane;
 #pragma unroll
     for (int s = 0; s < SA; ++s) an[s] = __ldg(cg + s * 32);
   }
-  for (int64_t g = g0 + warp; g < g1; g += kCtaWarps) {
+  // Ping-pong (DOA_SCAN_PP): warps 0-3 and 4-7 take turns on the DMMA pipe — a warp group issues
+  // its block's DMMAs, hands the pipe to the other group (named barriers 1/2) and runs its
+  // epilogue while the other group's DMMAs execute, so the pipe never idles on an epilogue phase
+  // that all warps would otherwise reach together.  Trip counts are CTA-uniform (warps past the
+  // chunk's last group still take their turns, without work).
+  const int wg = warp >> 2;
+  const int64_t nit = (g1 - g0 + kCtaWarps - 1) / kCtaWarps;
+  if (DOA_SCAN_PP && wg == 1) bar_arrive(1);
+  for (int64_t it = 0; it < nit; ++it) {
+    const int64_t g = g0 + warp + it * kCtaWarps;
+    const bool gv = g < g1;                                      // warp-uniform
     const double* cgc = coef + ((size_t)g * S) * 32 + lane;   // this group's A fragments
     double a[SA];
-    if (!STREAM_A) {
+    if (!STREAM_A && gv) {
 #pragma unroll
-      for (int s = 0; s < SA; ++s) a[s] = an[s];
-      if (g + kCtaWarps < g1) {                                // prefetch the next group's operands
+      for (int s = 0; s < SA; ++s) a[s] = DOA_SCAN_PF ? an[s] : __ldg(cgc + s * 32);
+      if (DOA_SCAN_PF && g + kCtaWarps < g1) {                                // prefetch the next group's operands
         const double* cg = coef + ((size_t)(g + kCtaWarps) * S) * 32 + lane;
 #pragma unroll
         for (int s = 0; s < SA; ++s) an[s] = __ldg(cg + s * 32);
       }
     }
     const int b = (int)(g * 8) + r;
-    const bool frame_ok = b < B;
+    const bool frame_ok = gv && b < B;
 #pragma unroll 1
     for (int k = 0; k < NB; ++k) {
       const int base = (blk0 + k) * (W - 2) - 1;
-      if (base + 1 >= (MIRROR ? H : L)) break;                 // warp-uniform
+      if (base + 1 >= (MIRROR ? H : L)) break;                 // CTA-uniform
       const double* Tk = Ts + (size_t)k * S * NA * 32 + lane;
       double acc[NA][2], aco[MIRROR ? NA : 1][2];
 #pragma unroll
@@ -350,40 +377,46 @@ __global__ void __launch_bounds__(kCtaWarps * 32, 2) scan_cta_kernel(const doubl
 #pragma unroll
         for (int t = 0; t < (MIRROR ? NA : 1); ++t) { aco[t][0] = 0.0; aco[t][1] = 0.0; }
       }
+      if (DOA_SCAN_PP) bar_sync(1 + wg);                         // my group's turn on the pipe
+      if (gv) {
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
-        const double av = STREAM_A ? __ldg(cgc + s * 32) : a[STREAM_A ? 0 : s];
-        if (!MIRROR || s < SE) {
+        for (int s = 0; s < S; ++s) {
+          const double av = STREAM_A ? __ldg(cgc + s * 32) : a[STREAM_A ? 0 : s];
+          if (!MIRROR || s < SE) {
 #pragma unroll
-          for (int t = 0; t < NA; ++t) dmma_884(acc[t][0], acc[t][1], av, Tk[(s * NA + t) * 32]);
-        } else {
+            for (int t = 0; t < NA; ++t) dmma_884(acc[t][0], acc[t][1], av, Tk[(s * NA + t) * 32]);
+          } else {
 #pragma unroll
-          for (int t = 0; t < (MIRROR ? NA : 1); ++t) dmma_884(aco[t][0], aco[t][1], av, Tk[(s * NA + t) * 32]);
+            for (int t = 0; t < (MIRROR ? NA : 1); ++t) dmma_884(aco[t][0], aco[t][1], av, Tk[(s * NA + t) * 32]);
+          }
         }
       }
+      if (DOA_SCAN_PP) bar_arrive(2 - wg);                       // hand the pipe to the other group
+      if (!gv) continue;
       if (!MIRROR) {
-        long long fi[NA][2];
+        long long fi[2 * NA];
 #pragma unroll
         for (int t = 0; t < NA; ++t) {
-          fi[t][0] = __double_as_longlong(acc[t][0]);
-          fi[t][1] = __double_as_longlong(acc[t][1]);
+          fi[2 * t] = __double_as_longlong(acc[t][0]);
+          fi[2 * t + 1] = __double_as_longlong(acc[t][1]);
         }
         scan_epilogue<NA, WRITE_P, false>(fi, lane, base, 1, L - 2, L - 1, L, b, frame_ok, cap, cnt, cidx, cf, P);
       } else {
-        long long fl[NA][2], fh[NA][2];
+        long long fl[2 * NA], fh[2 * NA];
 #pragma unroll
         for (int t = 0; t < NA; ++t)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const double ev = acc[t][e], od = aco[MIRROR ? t : 0][e];
-            fl[t][e] = __double_as_longlong(ev + od);           // f_i          = E + O
-            fh[t][e] = __double_as_longlong(ev - od);           // f_{L-1-i}    = E - O
+            fl[2 * t + e] = __double_as_longlong(ev + od);      // f_i          = E + O
+            fh[2 * t + e] = __double_as_longlong(ev - od);      // f_{L-1-i}    = E - O
           }
         scan_epilogue<NA, WRITE_P, false>(fl, lane, base, 1, H - 1, H - 1, L, b, frame_ok, cap, cnt, cidx, cf, P);
         scan_epilogue<NA, WRITE_P, true>(fh, lane, base, 1, L - 1 - H, L - 1 - H, L, b, frame_ok, cap, cnt, cidx, cf, P);
       }
     }
   }
+  if (DOA_SCAN_PP && wg == 0) bar_sync(1);                       // consume the other group's last hand-off
 }
 
 int sm_count() {

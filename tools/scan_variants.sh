@@ -1,11 +1,9 @@
 #!/bin/bash
-# A/B the scan kernel builds: default (2 CTAs/SM) vs DOA_SCAN_MINB=3.
-./tools/fp64_peaks > gpurun_out/fp64_peaks_mix.txt 2>&1
-for v in default build_variants/libdoa_minb3.so; do
+# A/B the scan kernel: bench c4 with the default libdoa.so and every build_variants/*.so (built
+# with -D overrides of the DOA_SCAN_* knobs in csrc/spectrum.cu); extra args = env settings for all.
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+for v in default build_variants/*.so; do
   if [ "$v" = default ]; then unset DOA_LIB; else export DOA_LIB=$PWD/$v; fi
-  echo "== $v" >> gpurun_out/scan_variants.txt
-  timeout 300 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline']['kernel_ms'], d['roofline']['frac'])" >> gpurun_out/scan_variants.txt 2>&1
+  printf "%-36s " "$v"
+  env "$@" timeout 300 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('value',round(d['value']),'ms/step',round(d['ms_per_step'],3),'spec_ms',round(d['roofline']['kernel_ms'],3),'frac',round(d['roofline']['frac'],3))"
 done
-unset DOA_LIB
-timeout 600 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu_v2.log 2>&1; tail -2 gpurun_out/pytest_gpu_v2.log
-cat gpurun_out/scan_variants.txt gpurun_out/fp64_peaks_mix.txt
