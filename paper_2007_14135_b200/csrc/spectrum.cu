@@ -206,6 +206,9 @@ constexpr int kCtaWarps = 8;
 #ifndef DOA_SCAN_PP
 #define DOA_SCAN_PP 1        // ping-pong the DMMA pipe between the two warp groups of a CTA
 #endif
+#ifndef DOA_SCAN_EO
+#define DOA_SCAN_EO 1        // mirrored scan: interleave the E and O k-steps in the DMMA sequence
+#endif
 #ifndef DOA_SCAN_PF
 #define DOA_SCAN_PF 1        // prefetch the next group's A fragments into registers
 #endif
@@ -379,15 +382,30 @@ __global__ void __launch_bounds__(kCtaWarps * 32, DOA_SCAN_MINB) scan_cta_kernel
       }
       if (DOA_SCAN_PP) bar_sync(1 + wg);                         // my group's turn on the pipe
       if (gv) {
+        if (!MIRROR || DOA_SCAN_EO == 0) {
 #pragma unroll
-        for (int s = 0; s < S; ++s) {
-          const double av = STREAM_A ? __ldg(cgc + s * 32) : a[STREAM_A ? 0 : s];
-          if (!MIRROR || s < SE) {
+          for (int s = 0; s < S; ++s) {
+            const double av = STREAM_A ? __ldg(cgc + s * 32) : a[STREAM_A ? 0 : s];
+            if (!MIRROR || s < SE) {
 #pragma unroll
-            for (int t = 0; t < NA; ++t) dmma_884(acc[t][0], acc[t][1], av, Tk[(s * NA + t) * 32]);
-          } else {
+              for (int t = 0; t < NA; ++t) dmma_884(acc[t][0], acc[t][1], av, Tk[(s * NA + t) * 32]);
+            } else {
 #pragma unroll
-            for (int t = 0; t < (MIRROR ? NA : 1); ++t) dmma_884(aco[t][0], aco[t][1], av, Tk[(s * NA + t) * 32]);
+              for (int t = 0; t < (MIRROR ? NA : 1); ++t) dmma_884(aco[t][0], aco[t][1], av, Tk[(s * NA + t) * 32]);
+            }
+          }
+        } else {
+          // E and O k-steps interleaved: 2 NA independent accumulator chains per step pair
+#pragma unroll
+          for (int s = 0; s < SE; ++s) {
+            const double ae = STREAM_A ? __ldg(cgc + s * 32) : a[STREAM_A ? 0 : s];
+            const bool has_o = SE + s < S;
+            const double ao = has_o ? (STREAM_A ? __ldg(cgc + (SE + s) * 32) : a[STREAM_A ? 0 : (SE + s < S ? SE + s : 0)]) : 0.0;
+#pragma unroll
+            for (int t = 0; t < NA; ++t) {
+              dmma_884(acc[t][0], acc[t][1], ae, Tk[(s * NA + t) * 32]);
+              if (has_o) dmma_884(aco[MIRROR ? t : 0][0], aco[MIRROR ? t : 0][1], ao, Tk[((SE + s) * NA + t) * 32]);
+            }
           }
         }
       }
