@@ -37,7 +37,7 @@ constexpr int kN = 16;            // padded order
 constexpr int kLd = 19;           // smem row stride (double2)
 constexpr int kEigWarps = 4;
 #ifndef DOA_EIG_MINB
-#define DOA_EIG_MINB 4
+#define DOA_EIG_MINB 5
 #endif
 
 __device__ __forceinline__ int aidx(int i, int j) { return i * kLd + (j ^ (i >> 1)); }
@@ -46,8 +46,17 @@ __device__ __forceinline__ int aidx(int i, int j) { return i * kLd + (j ^ (i >> 
 __device__ constexpr int kBlockOrder[28] = {7, 1, 25, 2, 24, 17, 20, 18, 12, 19, 13, 5, 21, 4,
                                              22, 3, 14, 8, 9, 11, 23, 26, 27, 16, 15, 10, 0, 6};
 
-struct Prm {
+// Rotation parameters of one slot pair.  Padded to 48 bytes (DOA_EIG_PRMPAD) so the eight pairs'
+// 16-byte halves fall in distinct shared-memory banks: phase 2b's loads (pairs k and k+4 in one
+// instruction) and phase 2a's (pairs rb, sb over 28 lanes) are single wavefronts.
+#ifndef DOA_EIG_PRMPAD
+#define DOA_EIG_PRMPAD 1
+#endif
+struct __align__(16) Prm {
   double c, s, er, ei;
+#if DOA_EIG_PRMPAD
+  double pad0, pad1;
+#endif
 };
 
 __device__ __forceinline__ double wsum(double v) {
@@ -81,6 +90,11 @@ __device__ __forceinline__ double rcp_pos(double x) {
   y = y * fma(-x, y, 2.0);
   y = y * fma(-x, y, 2.0);
   return y;
+}
+
+// x with its sign bit XORed (conjugation of a stored imaginary part): integer pipe, not FP64
+__device__ __forceinline__ double flip(double x, long long sgn) {
+  return __longlong_as_double(__double_as_longlong(x) ^ sgn);
 }
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -139,7 +153,7 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
   const int i0 = 2 * rb, i1 = 2 * rb + 1, j0 = 2 * sb, j1 = 2 * sb + 1;
   const int rd00 = aidx(i0, j0), rd01 = aidx(i0, j1), rd10 = aidx(i1, j0), rd11 = aidx(i1, j1);
   int wr[4];
-  double sg[4];                         // +1: store as is, -1: the permutation swapped the triangle
+  long long sg[4];                      // sign bit to XOR into Im: set when the permutation swapped the triangle
   {
     const int pr[2] = {cat_next(i0), cat_next(i1)}, pc[2] = {cat_next(j0), cat_next(j1)};
 #pragma unroll
@@ -148,7 +162,7 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
       for (int c = 0; c < 2; ++c) {
         const int x = pr[a], y = pc[c];
         wr[2 * a + c] = x < y ? aidx(x, y) : aidx(y, x);
-        sg[2 * a + c] = x < y ? 1.0 : -1.0;
+        sg[2 * a + c] = x < y ? 0LL : (long long)0x8000000000000000ULL;
       }
   }
   // phase-1 geometry (lanes 0..7): pair k = lane
@@ -241,10 +255,10 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
         const double2 n11 = make_double2(ps.s * b10.x + ps.c * t1.x, ps.s * b10.y + ps.c * t1.y);
         // rows (J_r^H): r0' = c r0 - s (conj(e) r1), r1' = s r0 + c (conj(e) r1)
         const double2 u0 = cmulc(er, n10), u1 = cmulc(er, n11);
-        An[wr[0]] = make_double2(pr.c * n00.x - pr.s * u0.x, sg[0] * (pr.c * n00.y - pr.s * u0.y));
-        An[wr[1]] = make_double2(pr.c * n01.x - pr.s * u1.x, sg[1] * (pr.c * n01.y - pr.s * u1.y));
-        An[wr[2]] = make_double2(pr.s * n00.x + pr.c * u0.x, sg[2] * (pr.s * n00.y + pr.c * u0.y));
-        An[wr[3]] = make_double2(pr.s * n01.x + pr.c * u1.x, sg[3] * (pr.s * n01.y + pr.c * u1.y));
+        An[wr[0]] = make_double2(pr.c * n00.x - pr.s * u0.x, flip(pr.c * n00.y - pr.s * u0.y, sg[0]));
+        An[wr[1]] = make_double2(pr.c * n01.x - pr.s * u1.x, flip(pr.c * n01.y - pr.s * u1.y, sg[1]));
+        An[wr[2]] = make_double2(pr.s * n00.x + pr.c * u0.x, flip(pr.s * n00.y + pr.c * u0.y, sg[2]));
+        An[wr[3]] = make_double2(pr.s * n01.x + pr.c * u1.x, flip(pr.s * n01.y + pr.c * u1.y, sg[3]));
       }
       // ---- phase 2b: V <- V J on this lane's four slot pairs (registers)
 #pragma unroll
