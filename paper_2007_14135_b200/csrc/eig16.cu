@@ -194,11 +194,18 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
       const double2* A = As[warp][cur];
       double2* An = As[warp][cur ^ 1];
       // ---- phase 1: rotation of slot pair k = lane & 7 + closed-form diagonal block.  Computed
-      // branch-free by all lanes (lanes 8..31 duplicate lanes 0..7); only lanes 0..7 store.
+      // branch-free by all lanes (lanes 8..31 on a dummy pair); only lanes 0..7 store.
       // Reciprocal square roots (MUFU seed + Newton, ~1 ulp) replace IEEE div/sqrt.
       {
-        const double2 axy = A[rxy];
-        const double axx = A[rxx].x, ayy = A[ryy].x;
+        // only lanes 0..7 read (shared-memory wavefronts scale with the active lanes); the
+        // others run the same instructions on a harmless dummy pair and store nothing
+        double2 axy = make_double2(1.0, 0.0);
+        double axx = 0.0, ayy = 0.0;
+        if (lane < 8) {
+          axy = A[rxy];
+          axx = A[rxx].x;
+          ayy = A[ryy].x;
+        }
         const double r2 = axy.x * axy.x + axy.y * axy.y;
         const bool rot = r2 > 1e-300;                         // a_xy ~ 0: identity rotation
         const double ir = rsqrt_pos(rot ? r2 : 1.0);          // 1/|a_xy|
