@@ -33,6 +33,12 @@ __device__ __forceinline__ float to_p32(double f) {
 // are split into M lags x H = 32/M vector-slices (M <= 16: every lane busy); the H partial sums
 // of a lag are combined in a fixed order (deterministic).
 constexpr int kCoefWarps = 4;
+#ifndef DOA_COEF_WAVES
+#define DOA_COEF_WAVES 2      // coef_mma_kernel CTAs = resident slots x waves (persistent warps)
+#endif
+#ifndef DOA_COEF_MMA
+#define DOA_COEF_MMA 1        // M <= 16: coefficients as a DMMA product C = X U^H + diagonal sums
+#endif
 
 __global__ void __launch_bounds__(kCoefWarps * 32) coef_kernel(const double* __restrict__ lam,
                                                               const double2* __restrict__ V, int64_t B, int M,
@@ -124,7 +130,7 @@ __global__ void __launch_bounds__(kCoefWarps * 32) coef_kernel(const double* __r
     if ((j >= M && j < JE) || j >= JE + M - 1) coef[coef_index(b, j, S)] = 0.0;
   if (lane == 0) {
     cnt[b] = 0;
-    if (info) info[b] |= flag;
+    if (info && flag) info[b] |= flag;           // no read-modify-write round trip when clean
   }
 }
 
@@ -165,6 +171,153 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
+}
+
+// S3 for M <= 16 on the FP64 tensor pipe.  C = X U^H with U = the noise vectors (columns of V)
+// and X = (w_j u_j) (weights only for EV; MN: the single vector w of Table 3 Step-3), i.e.
+//   C_re = X_re U_re^T + X_im U_im^T,   C_im = X_im U_re^T - X_re U_im^T   (16 x 16, inner dim j),
+// as DMMA m8n8k4 products over the upper 8x8 tiles (0,0), (0,1), (1,1) — at most 48 DMMAs per
+// frame — with the operand fragments read once from shared memory (U staged as re/im planes
+// [j][p], row stride 24 doubles).  The tiles go back through shared memory and lanes k < M add the
+// diagonal c_k = sum_p C[p][p+k] in ascending p.  Fixed orders throughout: deterministic.  Replaces
+// the lag-per-lane loop (coef_kernel) whose shared-memory traffic (~1000 wavefronts per frame)
+// bound it; this one moves ~150.
+constexpr int kCoefMmaWarps = 8;
+constexpr int kCoefMmaLd = 24;                         // plane row stride (doubles), = 8 mod 16
+constexpr int kCoefMmaPlane = 16 * kCoefMmaLd;         // doubles per plane
+
+__global__ void __launch_bounds__(kCoefMmaWarps * 32) coef_mma_kernel(const double* __restrict__ lam,
+                                                                      const double2* __restrict__ V, int64_t B,
+                                                                      int M, int D, int alg, double* __restrict__ coef,
+                                                                      int32_t* __restrict__ cnt,
+                                                                      int32_t* __restrict__ info) {
+  constexpr int ld = kCoefMmaLd;
+  extern __shared__ double cmsm[];                     // per warp: Ure, Uim planes; later C_re, C_im
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* Ure = cmsm + (size_t)warp * 2 * kCoefMmaPlane;
+  double* Uim = Ure + kCoefMmaPlane;
+  const int S = ksteps(M);
+  const int K = M - D;
+  const int nload = (alg == DOA_ALG_PHD) ? 1 : K;      // columns needed
+  // persistent warps: frame b, then b + stride, ...; the next frame's V loads are issued before
+  // the current frame is processed, so their latency overlaps the work
+  const int64_t stride = (int64_t)gridDim.x * kCoefMmaWarps;
+  int64_t b = (int64_t)blockIdx.x * kCoefMmaWarps + warp;
+  double2 tv[8];                                       // the whole 16 x 16 (j, p) slot grid, zero outside
+  auto load_v = [&](int64_t bb) {
+    const double2* Vb = V + (size_t)bb * M * M;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int e = lane + 32 * r, pp = e >> 4, j = e & 15;
+      tv[r] = (bb < B && pp < M && j < nload) ? __ldg(Vb + pp * M + j) : make_double2(0.0, 0.0);
+    }
+  };
+  load_v(b);
+  for (; b < B; b += stride) {
+  const double* lb = lam + (size_t)b * M;
+  int flag = 0;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int e = lane + 32 * r, pp = e >> 4, j = e & 15;
+    Ure[j * ld + pp] = tv[r].x;
+    Uim[j * ld + pp] = tv[r].y;
+  }
+  load_v(b + stride);
+  __syncwarp();
+  int nv = (alg == DOA_ALG_MUSIC || alg == DOA_ALG_EV) ? K : 1;
+  // EV weights w_j = 1/lambda_j (Q1), clamped at 100 eps lambda_max (DEGENERATE)
+  double wj[4] = {1.0, 1.0, 1.0, 1.0};                 // weight of row j = 4J + lane%4 of X
+  if (alg == DOA_ALG_EV) {
+    const double lfloor = 100.0 * DBL_EPSILON * fmax(lb[M - 1], 0.0);
+    for (int j = 0; j < K; ++j) if (lb[j] <= lfloor) flag |= DOA_INFO_DEGENERATE;
+#pragma unroll
+    for (int J = 0; J < 4; ++J) {
+      const int j = 4 * J + (lane & 3);
+      wj[J] = j < K ? (lb[j] <= lfloor ? (lfloor > 0.0 ? 1.0 / lfloor : 1.0) : 1.0 / lb[j]) : 0.0;
+    }
+  } else if (alg == DOA_ALG_MN) {
+    // w = P_n e1 / (e1^H P_n e1): P_n e1 = sum_j e_j conj(e_j[0]), e1^H P_n e1 = sum_j |e_j[0]|^2
+    double p0 = 0.0;
+    for (int j = 0; j < K; ++j) p0 += Ure[j * ld] * Ure[j * ld] + Uim[j * ld] * Uim[j * ld];
+    const bool degen = !(p0 > 100.0 * DBL_EPSILON);
+    if (degen) flag |= DOA_INFO_DEGENERATE;
+    const double lp = degen ? 1.0 : 1.0 / p0;
+    double pr = 0.0, pi = 0.0;
+    if (lane < M)
+      for (int j = 0; j < K; ++j) {
+        const double er = Ure[j * ld + lane], ei = Uim[j * ld + lane], e0r = Ure[j * ld], e0i = Uim[j * ld];
+        pr += er * e0r + ei * e0i;                     // e_j[i] * conj(e_j[0])
+        pi += ei * e0r - er * e0i;
+      }
+    __syncwarp();
+    if (lane < 16) {
+      Ure[lane] = degen ? pr : pr * lp;                // vector 0 <- w (zero beyond M)
+      Uim[lane] = degen ? pi : pi * lp;
+    }
+    __syncwarp();
+  }
+  const int nJ = (nv + 3) >> 2;                        // k-steps over j
+  const int r4 = lane & 3, c8 = lane >> 2;
+  // fragments: A[p][j] = x_j[p] (row p = 8P + c8, col j = 4J + r4); B[j][q] = u_j[q] (q = 8Q + c8)
+  double ar[2][4], ai[2][4], br[2][4], bi[2][4];
+#pragma unroll
+  for (int J = 0; J < 4; ++J)
+#pragma unroll
+    for (int P = 0; P < 2; ++P) {
+      const int o = (4 * J + r4) * ld + 8 * P + c8;
+      const bool ok = 4 * J + r4 < nv;                   // rows j >= nv (e.g. MN beyond w) are zero
+      const double ur = ok ? Ure[o] : 0.0, ui = ok ? Uim[o] : 0.0;
+      br[P][J] = ur;
+      bi[P][J] = ui;
+      ar[P][J] = wj[J] * ur;
+      ai[P][J] = wj[J] * ui;
+    }
+  // upper tiles (P, Q) = (0,0), (0,1), (1,1); C_re, C_im accumulators
+  double cr[3][2], ci[3][2];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) { cr[t][0] = cr[t][1] = ci[t][0] = ci[t][1] = 0.0; }
+#pragma unroll
+  for (int J = 0; J < 4; ++J) {
+    if (J >= nJ) break;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const int P = t == 2 ? 1 : 0, Q = t == 0 ? 0 : 1;
+      dmma_884(cr[t][0], cr[t][1], ar[P][J], br[Q][J]);
+      dmma_884(cr[t][0], cr[t][1], ai[P][J], bi[Q][J]);
+      dmma_884(ci[t][0], ci[t][1], ai[P][J], br[Q][J]);
+      dmma_884(ci[t][0], ci[t][1], -ar[P][J], bi[Q][J]);
+    }
+  }
+  __syncwarp();                                        // every lane has its fragments: reuse the planes
+  double* Cre = Ure;                                   // C[p][q] at p * ld + q
+  double* Cim = Uim;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const int P = t == 2 ? 1 : 0, Q = t == 0 ? 0 : 1;
+    const int o = (8 * P + c8) * ld + 8 * Q + 2 * r4;
+    Cre[o] = cr[t][0]; Cre[o + 1] = cr[t][1];
+    Cim[o] = ci[t][0]; Cim[o + 1] = ci[t][1];
+  }
+  __syncwarp();
+  if (lane < M) {
+    const int k = lane;
+    double sr = 0.0, si = 0.0;
+    for (int pp = 0; pp + k < M; ++pp) { sr += Cre[pp * ld + pp + k]; si += Cim[pp * ld + pp + k]; }
+    if (k == 0) coef[coef_index(b, 0, S)] = sr;
+    else {
+      coef[coef_index(b, coef_cos(k), S)] = 2.0 * sr;
+      coef[coef_index(b, coef_sin(M, k), S)] = 2.0 * si;
+    }
+  }
+  const int JE = 4 * ksteps_even(M);
+  for (int j = lane; j < 4 * S; j += 32)                                                // K padding
+    if ((j >= M && j < JE) || j >= JE + M - 1) coef[coef_index(b, j, S)] = 0.0;
+  if (lane == 0) {
+    cnt[b] = 0;
+    if (info && flag) info[b] |= flag;           // no read-modify-write round trip when clean
+  }
+  __syncwarp();                                        // C planes are read above before the next stores
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -518,7 +671,7 @@ __global__ void __launch_bounds__(128) select_kernel(int64_t B, int D, int cap, 
     int fl = 0;
     if (nraw > cap) fl |= DOA_INFO_CAND_OVERFLOW;
     if (n < D) fl |= DOA_INFO_UNDERDETERMINED;
-    info[b] |= fl;
+    if (fl) info[b] |= fl;
   }
 }
 
@@ -527,6 +680,26 @@ __global__ void __launch_bounds__(128) select_kernel(int64_t B, int D, int cap, 
 cudaError_t launch_coef(const doa_plan_s* p, const double* lam, const double* V, int64_t B, int32_t* info,
                         cudaStream_t s) {
   const int M = p->M;
+  count_launch();
+  if (M <= 16 && DOA_COEF_MMA) {
+    const size_t smem = (size_t)kCoefMmaWarps * 2 * kCoefMmaPlane * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(coef_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    static int occ = 0;
+    if (!occ) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, coef_mma_kernel, kCoefMmaWarps * 32, smem);
+      if (occ < 1) occ = 1;
+    }
+    int64_t nb = (B + kCoefMmaWarps - 1) / kCoefMmaWarps;
+    const int64_t slots = (int64_t)sm_count() * occ * DOA_COEF_WAVES;
+    if (nb > slots) nb = slots;
+    coef_mma_kernel<<<(unsigned)nb, kCoefMmaWarps * 32, smem, s>>>(
+        lam, reinterpret_cast<const double2*>(V), B, M, p->D, p->alg, p->coef, p->cnt, info);
+    return cudaGetLastError();
+  }
   const int wpc = M <= 32 ? kCoefWarps : 2;
   const size_t smem = (size_t)wpc * (M * (M + 1) + 32) * sizeof(double2);
   static bool attr = false;
@@ -535,7 +708,6 @@ cudaError_t launch_coef(const doa_plan_s* p, const double* lam, const double* V,
                          (int)(2 * (kMaxM * (kMaxM + 1) + 32) * sizeof(double2)));
     attr = true;
   }
-  count_launch();
   coef_kernel<<<(unsigned)((B + wpc - 1) / wpc), wpc * 32, smem, s>>>(lam, reinterpret_cast<const double2*>(V), B, M,
                                                                        p->D, p->alg, p->coef, p->cnt, info);
   return cudaGetLastError();
