@@ -178,12 +178,12 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 //   C_re = X_re U_re^T + X_im U_im^T,   C_im = X_im U_re^T - X_re U_im^T   (16 x 16, inner dim j),
 // as DMMA m8n8k4 products over the upper 8x8 tiles (0,0), (0,1), (1,1) — at most 48 DMMAs per
 // frame — with the operand fragments read once from shared memory (U staged as re/im planes
-// [j][p], row stride 24 doubles).  The tiles go back through shared memory and lanes k < M add the
+// [j][p], row stride 20 doubles: conflict-free staging stores and fragment loads).  The tiles go back through shared memory and lanes k < M add the
 // diagonal c_k = sum_p C[p][p+k] in ascending p.  Fixed orders throughout: deterministic.  Replaces
 // the lag-per-lane loop (coef_kernel) whose shared-memory traffic (~1000 wavefronts per frame)
 // bound it; this one moves ~150.
 constexpr int kCoefMmaWarps = 8;
-constexpr int kCoefMmaLd = 24;                         // plane row stride (doubles), = 8 mod 16
+constexpr int kCoefMmaLd = 20;                         // plane row stride (doubles), = 4 mod 16: conflict-free fragments
 constexpr int kCoefMmaPlane = 16 * kCoefMmaLd;         // doubles per plane
 
 __global__ void __launch_bounds__(kCoefMmaWarps * 32) coef_mma_kernel(const double* __restrict__ lam,
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kCoefMmaWarps * 32) coef_mma_kernel(const doub
     const double2* Vb = V + (size_t)bb * M * M;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-      const int e = lane + 32 * r, pp = e >> 4, j = e & 15;
+      const int e = lane + 32 * r, pp = e & 15, j = e >> 4;
       tv[r] = (bb < B && pp < M && j < nload) ? __ldg(Vb + pp * M + j) : make_double2(0.0, 0.0);
     }
   };
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kCoefMmaWarps * 32) coef_mma_kernel(const doub
   int flag = 0;
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
-    const int e = lane + 32 * r, pp = e >> 4, j = e & 15;
+    const int e = lane + 32 * r, pp = e & 15, j = e >> 4;
     Ure[j * ld + pp] = tv[r].x;
     Uim[j * ld + pp] = tv[r].y;
   }
@@ -301,8 +301,16 @@ __global__ void __launch_bounds__(kCoefMmaWarps * 32) coef_mma_kernel(const doub
   __syncwarp();
   if (lane < M) {
     const int k = lane;
+    double dr[16], di[16];                             // all loads first, then the adds in ascending p
+#pragma unroll
+    for (int pp = 0; pp < 16; ++pp) {
+      const bool ok = pp + k < M;
+      dr[pp] = ok ? Cre[pp * ld + pp + k] : 0.0;
+      di[pp] = ok ? Cim[pp * ld + pp + k] : 0.0;
+    }
     double sr = 0.0, si = 0.0;
-    for (int pp = 0; pp + k < M; ++pp) { sr += Cre[pp * ld + pp + k]; si += Cim[pp * ld + pp + k]; }
+#pragma unroll
+    for (int pp = 0; pp < 16; ++pp) { sr += dr[pp]; si += di[pp]; }
     if (k == 0) coef[coef_index(b, 0, S)] = sr;
     else {
       coef[coef_index(b, coef_cos(k), S)] = 2.0 * sr;
