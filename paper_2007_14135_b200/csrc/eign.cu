@@ -62,6 +62,16 @@ struct EigN {
 };
 
 template <int N>
+__device__ __forceinline__ int prm_slot(int p) { return (p & 3) * EigN<N>::Q + (p >> 2); }
+template <int N>
+__device__ __forceinline__ PrmN load_prm(const double2* cs, const double2* ee, int p) {
+  const double2 a = cs[prm_slot<N>(p)], e = ee[prm_slot<N>(p)];
+  PrmN r;
+  r.c = a.x; r.s = a.y; r.er = e.x; r.ei = e.y;
+  return r;
+}
+
+template <int N>
 __device__ __forceinline__ int aidxN(int i, int j) { return i * EigN<N>::LD + (j ^ (i >> 1)); }
 
 template <int N>
@@ -86,7 +96,9 @@ __global__ void __launch_bounds__(EigN<N>::T, 1) eigN_kernel(const double2* __re
   using E = EigN<N>;
   constexpr int LD = E::LD, Q = E::Q, NP = E::NP, NBLK = E::NBLK;
   extern __shared__ double2 As[];                                   // [2][N * LD]
-  __shared__ PrmN prm[NP];
+  // rotation parameters as two arrays of 16-byte entries, pair p at slot (p % 4) * Q + p / 4: phase
+  // 2b's lanes (group h reads pairs 4h + kk) hit consecutive entries, one wavefront per load
+  __shared__ double2 prm_cs[NP], prm_ee[NP];
   __shared__ double red[32];
   __shared__ int rank_s[N];
   const int tid = threadIdx.x;
@@ -180,7 +192,8 @@ __global__ void __launch_bounds__(EigN<N>::T, 1) eigN_kernel(const double2* __re
         p.s = t * p.c;
         p.er = rot ? axy.x * ir : 1.0;
         p.ei = rot ? -axy.y * ir : 0.0;
-        prm[tid] = p;
+        prm_cs[prm_slot<N>(tid)] = make_double2(p.c, p.s);
+        prm_ee[prm_slot<N>(tid)] = make_double2(p.er, p.ei);
         An[wxx] = make_double2(axx - t * rr, 0.0);
         An[wyy] = make_double2(ayy + t * rr, 0.0);
         An[wxy] = make_double2(0.0, 0.0);
@@ -188,7 +201,7 @@ __global__ void __launch_bounds__(EigN<N>::T, 1) eigN_kernel(const double2* __re
       __syncthreads();
       // ---- phase 2a: off-diagonal block (rb, sb)
       if (has_blk) {
-        const PrmN pr = prm[rb], ps = prm[sb];
+        const PrmN pr = load_prm<N>(prm_cs, prm_ee, rb), ps = load_prm<N>(prm_cs, prm_ee, sb);
         const double2 b00 = A[rd00], b01 = A[rd01], b10 = A[rd10], b11 = A[rd11];
         const double2 es = make_double2(ps.er, ps.ei), er = make_double2(pr.er, pr.ei);
         const double2 t0 = cmulN(es, b01), t1 = cmulN(es, b11);
@@ -205,7 +218,7 @@ __global__ void __launch_bounds__(EigN<N>::T, 1) eigN_kernel(const double2* __re
       // ---- phase 2b: V <- V J on this thread's four slot pairs
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
-        const PrmN p = prm[4 * h + kk];
+        const PrmN p = load_prm<N>(prm_cs, prm_ee, 4 * h + kk);
         const double2 vx = v[2 * kk], vy = v[2 * kk + 1];
         const double2 t = cmulN(make_double2(p.er, p.ei), vy);
         v[2 * kk] = make_double2(p.c * vx.x - p.s * t.x, p.c * vx.y - p.s * t.y);
