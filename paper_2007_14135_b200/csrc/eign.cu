@@ -5,7 +5,7 @@
 //   * circle-method round robin in fixed slots (N/2 disjoint pairs per round) with the
 //     "caterpillar" permutation pi (slot 0 fixed, slots 1..N-1 on one (N-1)-cycle), folded into
 //     the smem store addresses; pi^(N-1) = id, so slots equal indices again after every sweep;
-//   * A = upper triangle in shared memory, double-buffered, layout (i, j) -> i*LD + (j ^ i/2);
+//   * A = upper triangle in shared memory, double-buffered, swizzled layout aidxN (conflict search);
 //   * phase 1 (threads < N/2): rotation parameters of the N/2 pairs + closed-form diagonal blocks;
 //     phase 2: thread t < (N/2)(N/2-1)/2 updates off-diagonal 2x2 block t (B <- J_r^H B J_s);
 //     every thread updates its 8 V entries in registers (V <- V J);
@@ -54,15 +54,19 @@ __device__ __forceinline__ int cat_nextN(int s, int N) {
 
 template <int N>
 struct EigN {
-  static constexpr int LD = N + 3;
+  static constexpr int LD = N + 2;
   static constexpr int Q = N / 8;                 // V groups of 8 slots per row
   static constexpr int T = N * Q;                 // threads
   static constexpr int NP = N / 2;                // pairs per round
   static constexpr int NBLK = NP * (NP - 1) / 2;  // off-diagonal 2x2 blocks
 };
 
+// Shared memory serves a 16-byte-per-lane load in quarter-warps of 8 lanes, which must hit distinct
+// 16-byte bank quads (slot % 8).  Phase 2b's quarter-warps read pairs 4h + kk, h = 0..7, and phase
+// 2a's read about 8 consecutive pairs sb; the swizzle slot = p ^ ((p >> 3) & 3) keeps both
+// conflict-free (2a: at most 2-way when the 8 pairs straddle a multiple of 8).
 template <int N>
-__device__ __forceinline__ int prm_slot(int p) { return (p & 3) * EigN<N>::Q + (p >> 2); }
+__device__ __forceinline__ int prm_slot(int p) { return p ^ ((p >> 3) & 3); }
 template <int N>
 __device__ __forceinline__ PrmN load_prm(const double2* cs, const double2* ee, int p) {
   const double2 a = cs[prm_slot<N>(p)], e = ee[prm_slot<N>(p)];
@@ -71,8 +75,14 @@ __device__ __forceinline__ PrmN load_prm(const double2* cs, const double2* ee, i
   return r;
 }
 
+// A layout: row stride N + 2, columns XOR-swizzled within aligned groups of 8 by (j/2) ^ 2(i/2);
+// chosen by an offline search over the 2a block loads and permuted stores (quarter-warps of 8
+// lanes, 16-byte entries): 667 wavefronts per round at N = 64 against 993 for i*(N+3) + (j ^ i/2)
+// and an ideal of 496.
 template <int N>
-__device__ __forceinline__ int aidxN(int i, int j) { return i * EigN<N>::LD + (j ^ (i >> 1)); }
+__device__ __forceinline__ int aidxN(int i, int j) {
+  return i * EigN<N>::LD + (j ^ ((((j >> 1) & 7) ^ ((i >> 1) * 2)) & 7));
+}
 
 template <int N>
 __device__ __forceinline__ double block_sum(double v, double* red) {
@@ -96,8 +106,7 @@ __global__ void __launch_bounds__(EigN<N>::T, 1) eigN_kernel(const double2* __re
   using E = EigN<N>;
   constexpr int LD = E::LD, Q = E::Q, NP = E::NP, NBLK = E::NBLK;
   extern __shared__ double2 As[];                                   // [2][N * LD]
-  // rotation parameters as two arrays of 16-byte entries, pair p at slot (p % 4) * Q + p / 4: phase
-  // 2b's lanes (group h reads pairs 4h + kk) hit consecutive entries, one wavefront per load
+  // rotation parameters as two arrays of 16-byte entries (c, s) and (er, ei), pair p at prm_slot(p)
   __shared__ double2 prm_cs[NP], prm_ee[NP];
   __shared__ double red[32];
   __shared__ int rank_s[N];
