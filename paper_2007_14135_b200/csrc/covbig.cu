@@ -27,7 +27,8 @@ template <int MP>
 struct CovBig {
   static constexpr int RB = 2 * MP / 8;                  // 8-row blocks of Y
   static constexpr int WARPS = RB / 2;
-  static constexpr int XS = MP + 8;                      // plane row stride (doubles)
+  static constexpr int XS = MP + 4;                      // plane row stride (doubles), = 4 mod 16: the
+                                                         // fragment loads (rows n = 4ks + q, cols r) hit 16 distinct bank pairs per half-warp
   static constexpr int GS = 2 * MP + 1;                  // Gram row stride (doubles)
   static constexpr size_t STAGE = (size_t)2 * kChunk * XS;               // doubles per stage (Re + Im)
   static constexpr size_t SMEM = (2 * STAGE > (size_t)(2 * MP) * GS ? 2 * STAGE : (size_t)(2 * MP) * GS) * 8;
@@ -53,23 +54,35 @@ __global__ void __launch_bounds__(CovBig<MP>::WARPS * 32, 1) covbig_kernel(const
   for (int J = 0; J < RB; ++J) { acc1[J][0] = acc1[J][1] = 0.0; acc2[J][0] = acc2[J][1] = 0.0; }
 
   const int64_t nchunks = (N + kChunk - 1) / kChunk;
-  auto stage = [&](int64_t c, int buf) {
-    double* Xr = sm + buf * C::STAGE;
-    double* Xi = Xr + kChunk * XS;
+  // Software pipeline over snapshot chunks: the next chunk's global loads are issued into
+  // registers before this chunk's DMMAs and stored (converted) into the other buffer after them,
+  // so their latency overlaps the math instead of stalling the same warps.
+  constexpr int PER = kChunk * MP / T;                   // elements per thread per chunk
+  float2 pre[PER];
+  auto load = [&](int64_t c) {
     const int64_t n0 = c * kChunk;
-    for (int e = tid; e < kChunk * MP; e += T) {
-      const int n = e / MP, m = e - (e / MP) * MP;
-      float2 x = make_float2(0.f, 0.f);
-      if (m < M && n0 + n < N) x = Xb[(size_t)(n0 + n) * M + m];
-      Xr[n * XS + m] = (double)x.x;
-      Xi[n * XS + m] = (double)x.y;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + u * T, n = e / MP, m = e - (e / MP) * MP;
+      pre[u] = (m < M && n0 + n < N) ? __ldg(Xb + (size_t)(n0 + n) * M + m) : make_float2(0.f, 0.f);
     }
   };
-  stage(0, 0);
+  auto store = [&](int buf) {
+    double* Xr = sm + buf * C::STAGE;
+    double* Xi = Xr + kChunk * XS;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + u * T, n = e / MP, m = e - (e / MP) * MP;
+      Xr[n * XS + m] = (double)pre[u].x;
+      Xi[n * XS + m] = (double)pre[u].y;
+    }
+  };
+  load(0);
+  store(0);
   __syncthreads();
   for (int64_t c = 0; c < nchunks; ++c) {
     const int buf = (int)(c & 1);
-    if (c + 1 < nchunks) stage(c + 1, buf ^ 1);            // other buffer: freed by the last sync
+    if (c + 1 < nchunks) load(c + 1);
     const double* Xs = sm + buf * C::STAGE;
 #pragma unroll 2
     for (int ks = 0; ks < kChunk / 4; ++ks) {
@@ -85,6 +98,7 @@ __global__ void __launch_bounds__(CovBig<MP>::WARPS * 32, 1) covbig_kernel(const
         if (J >= I2 && I2 != I1) dmma_b(acc2[J][0], acc2[J][1], a2, fr[J]);
       }
     }
+    if (c + 1 < nchunks) store(buf ^ 1);                 // other buffer: freed by the last sync
     __syncthreads();
   }
   // tiles -> shared Gram matrix (reuses the staging space), mirrored
