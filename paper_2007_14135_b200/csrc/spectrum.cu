@@ -328,6 +328,144 @@ __global__ void __launch_bounds__(kCoefMmaWarps * 32) coef_mma_kernel(const doub
   }
 }
 
+// S3 for 16 < M <= 64: the same DMMA formulation with one CTA (8 warps) per frame.  MP = 32 / 64
+// padded rows, TP = MP/8 tile rows; the TP(TP+1)/2 upper 8x8 tiles of C = X U^H are dealt
+// round-robin to the warps; per k-step J over the noise vectors every warp loads the fragments of
+// its tiles' row / column blocks from the shared re/im planes and issues 4 DMMAs per tile.  The
+// tiles then overwrite the planes and threads k < M add the diagonals in ascending p.
+constexpr int kCoefBigWarps = 8;
+template <int MP>
+struct CoefBig {
+  static constexpr int TP = MP / 8;
+  static constexpr int NT = TP * (TP + 1) / 2;           // upper tiles
+  static constexpr int TPW = (NT + kCoefBigWarps - 1) / kCoefBigWarps;   // tiles per warp (max)
+  static constexpr int LD = MP + 4;                      // plane row stride (doubles), = 4 mod 16
+  static constexpr int PLANE = MP * LD;                  // rows j < MP (K < M <= MP)
+  static constexpr size_t SMEM = (size_t)2 * PLANE * sizeof(double) + MP * sizeof(double);
+};
+
+template <int MP>
+__global__ void __launch_bounds__(kCoefBigWarps * 32) coef_big_kernel(const double* __restrict__ lam,
+                                                                      const double2* __restrict__ V, int64_t B,
+                                                                      int M, int D, int alg,
+                                                                      double* __restrict__ coef,
+                                                                      int32_t* __restrict__ cnt,
+                                                                      int32_t* __restrict__ info) {
+  using C = CoefBig<MP>;
+  constexpr int ld = C::LD, TP = C::TP, NT = C::NT, TPW = C::TPW, T = kCoefBigWarps * 32;
+  extern __shared__ double cbsm[];
+  double* Ure = cbsm;                                    // [j][p]
+  double* Uim = Ure + C::PLANE;
+  double* wsh = Uim + C::PLANE;                          // [MP] EV weights
+  __shared__ int flag_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t b = blockIdx.x;
+  const double2* Vb = V + (size_t)b * M * M;
+  const double* lb = lam + (size_t)b * M;
+  const int S = ksteps(M);
+  const int K = M - D;
+  const int nload = (alg == DOA_ALG_PHD) ? 1 : K;
+  if (tid == 0) flag_s = 0;
+  // stage the noise vectors: V[p][j] -> planes [j][p] (coalesced global reads along j)
+  for (int e = tid; e < MP * MP; e += T) {
+    const int pp = e / MP, j = e - (e / MP) * MP;
+    const double2 v = (pp < M && j < nload) ? __ldg(Vb + pp * M + j) : make_double2(0.0, 0.0);
+    Ure[j * ld + pp] = v.x;
+    Uim[j * ld + pp] = v.y;
+  }
+  if (alg == DOA_ALG_EV && tid < MP) {
+    const double lfloor = 100.0 * DBL_EPSILON * fmax(lb[M - 1], 0.0);
+    double w = 0.0;
+    if (tid < K) {
+      w = lb[tid] <= lfloor ? (lfloor > 0.0 ? 1.0 / lfloor : 1.0) : 1.0 / lb[tid];
+      if (lb[tid] <= lfloor) atomicOr(&flag_s, DOA_INFO_DEGENERATE);
+    }
+    wsh[tid] = w;
+  }
+  __syncthreads();
+  int nv = (alg == DOA_ALG_MUSIC || alg == DOA_ALG_EV) ? K : 1;
+  if (alg == DOA_ALG_MN) {
+    double p0 = 0.0;
+    for (int j = 0; j < K; ++j) p0 += Ure[j * ld] * Ure[j * ld] + Uim[j * ld] * Uim[j * ld];
+    const bool degen = !(p0 > 100.0 * DBL_EPSILON);
+    const double lp = degen ? 1.0 : 1.0 / p0;
+    double pr = 0.0, pi = 0.0;
+    if (tid < M)
+      for (int j = 0; j < K; ++j) {
+        const double er = Ure[j * ld + tid], ei = Uim[j * ld + tid], e0r = Ure[j * ld], e0i = Uim[j * ld];
+        pr += er * e0r + ei * e0i;                       // e_j[i] * conj(e_j[0])
+        pi += ei * e0r - er * e0i;
+      }
+    __syncthreads();
+    if (tid < MP) {
+      Ure[tid] = degen ? pr : pr * lp;                   // vector 0 <- w (zero beyond M)
+      Uim[tid] = degen ? pi : pi * lp;
+    }
+    if (tid == 0 && degen) flag_s |= DOA_INFO_DEGENERATE;
+    __syncthreads();
+  }
+  const int nJ = (nv + 3) >> 2;
+  const int r4 = lane & 3, c8 = lane >> 2;
+  const bool ev = alg == DOA_ALG_EV;
+  int tP[TPW], tQ[TPW];
+#pragma unroll
+  for (int u = 0; u < TPW; ++u) {
+    int t = warp + u * kCoefBigWarps, P = 0;
+    if (t >= NT) t = -1;
+    int rem = t < 0 ? 0 : t;
+    while (rem >= TP - P) { rem -= TP - P; ++P; }      // row-major upper tiles: row P has TP - P tiles
+    tP[u] = t < 0 ? -1 : P;
+    tQ[u] = P + rem;
+  }
+  double cr[TPW][2], ci[TPW][2];
+#pragma unroll
+  for (int u = 0; u < TPW; ++u) { cr[u][0] = cr[u][1] = ci[u][0] = ci[u][1] = 0.0; }
+  for (int J = 0; J < nJ; ++J) {
+    const int j = 4 * J + r4;
+    const bool ok = j < nv;
+    const double w = ev ? (ok ? wsh[j] : 0.0) : 1.0;
+#pragma unroll
+    for (int u = 0; u < TPW; ++u) {
+      if (tP[u] < 0) continue;                           // warp-uniform
+      const int oa = j * ld + 8 * tP[u] + c8, ob = j * ld + 8 * tQ[u] + c8;
+      const double ur = ok ? Ure[ob] : 0.0, ui = ok ? Uim[ob] : 0.0;
+      const double xr = ok ? w * Ure[oa] : 0.0, xi = ok ? w * Uim[oa] : 0.0;
+      dmma_884(cr[u][0], cr[u][1], xr, ur);
+      dmma_884(cr[u][0], cr[u][1], xi, ui);
+      dmma_884(ci[u][0], ci[u][1], xi, ur);
+      dmma_884(ci[u][0], ci[u][1], -xr, ui);
+    }
+  }
+  __syncthreads();                                       // all fragments read: the planes become C
+  double* Cre = Ure;                                     // C[p][q] at p * ld + q
+  double* Cim = Uim;
+#pragma unroll
+  for (int u = 0; u < TPW; ++u) {
+    if (tP[u] < 0) continue;
+    const int o = (8 * tP[u] + c8) * ld + 8 * tQ[u] + 2 * r4;
+    Cre[o] = cr[u][0]; Cre[o + 1] = cr[u][1];
+    Cim[o] = ci[u][0]; Cim[o + 1] = ci[u][1];
+  }
+  __syncthreads();
+  if (tid < M) {
+    const int k = tid;
+    double sr = 0.0, si = 0.0;
+    for (int pp = 0; pp + k < M; ++pp) { sr += Cre[pp * ld + pp + k]; si += Cim[pp * ld + pp + k]; }
+    if (k == 0) coef[coef_index(b, 0, S)] = sr;
+    else {
+      coef[coef_index(b, coef_cos(k), S)] = 2.0 * sr;
+      coef[coef_index(b, coef_sin(M, k), S)] = 2.0 * si;
+    }
+  }
+  const int JE = 4 * ksteps_even(M);
+  for (int j = tid; j < 4 * S; j += T)                                                  // K padding
+    if ((j >= M && j < JE) || j >= JE + M - 1) coef[coef_index(b, j, S)] = 0.0;
+  if (tid == 0) {
+    cnt[b] = 0;
+    if (info && flag_s) info[b] |= flag_s;
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
 // S4-S6: the scan on the FP64 tensor pipe (mma.sync m8n8k4 f64).
 //
@@ -706,6 +844,21 @@ cudaError_t launch_coef(const doa_plan_s* p, const double* lam, const double* V,
     if (nb > slots) nb = slots;
     coef_mma_kernel<<<(unsigned)nb, kCoefMmaWarps * 32, smem, s>>>(
         lam, reinterpret_cast<const double2*>(V), B, M, p->D, p->alg, p->coef, p->cnt, info);
+    return cudaGetLastError();
+  }
+  if (DOA_COEF_MMA) {
+    static bool attr_big = false;
+    if (!attr_big) {
+      cudaFuncSetAttribute(coef_big_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CoefBig<32>::SMEM);
+      cudaFuncSetAttribute(coef_big_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CoefBig<64>::SMEM);
+      attr_big = true;
+    }
+    auto go = [&](auto kern, size_t smem) {
+      kern<<<(unsigned)B, kCoefBigWarps * 32, smem, s>>>(lam, reinterpret_cast<const double2*>(V), B, M, p->D, p->alg,
+                                                         p->coef, p->cnt, info);
+    };
+    if (M <= 32) go(coef_big_kernel<32>, CoefBig<32>::SMEM);
+    else go(coef_big_kernel<64>, CoefBig<64>::SMEM);
     return cudaGetLastError();
   }
   const int wpc = M <= 32 ? kCoefWarps : 2;
