@@ -12,8 +12,10 @@
 //   double-buffered: each round reads buffer `cur` and writes every upper element of buffer `nxt`
 //   at its PERMUTED position (pi(i), pi(j)) (conjugated when the permutation swaps the triangle),
 //   so the permutation costs only static per-lane store addresses.  The smem layout
-//   (i, j) -> i*19 + (j ^ (i/2)) and the lane -> block order below minimise bank conflicts of the
-//   block reads / permuted writes (searched offline: 48 wavefronts per round vs 104 row-major).
+//   (i, j) -> i*17 + (j ^ (i/2)) and the lane -> block order below minimise bank conflicts of the
+//   block reads / permuted writes and the phase-1 accesses (offline search with the quarter-warp
+//   model of 16-byte accesses: 47 wavefronts per round for these 14 instructions vs 57 for the
+//   previous i*19 layout, ideal 40).
 //     phase 1  lanes 0..7   : rotation of slot pair k from (a_xx, a_yy, a_xy) and the closed-form
 //                             2x2 diagonal block (a_xx - t|a_xy|, a_yy + t|a_xy|, 0)
 //                             (Golub & Van Loan sym.schur2 after the phase rotation).
@@ -34,7 +36,7 @@ namespace doa {
 namespace {
 
 constexpr int kN = 16;            // padded order
-constexpr int kLd = 19;           // smem row stride (double2)
+constexpr int kLd = 17;           // smem row stride (double2)
 constexpr int kEigWarps = 4;
 #ifndef DOA_EIG_MINB
 #define DOA_EIG_MINB 5
@@ -43,8 +45,8 @@ constexpr int kEigWarps = 4;
 __device__ __forceinline__ int aidx(int i, int j) { return i * kLd + (j ^ (i >> 1)); }
 
 // lane -> off-diagonal slot-pair block (index into the row-major list of r < s pairs)
-__device__ constexpr int kBlockOrder[28] = {7, 1, 25, 2, 24, 17, 20, 18, 12, 19, 13, 5, 21, 4,
-                                             22, 3, 14, 8, 9, 11, 23, 26, 27, 16, 15, 10, 0, 6};
+__device__ constexpr int kBlockOrder[28] = {14, 11, 10, 16, 13, 8, 25, 15, 4, 6, 19, 12, 21, 26,
+                                             1, 17, 18, 7, 23, 24, 22, 20, 9, 27, 3, 2, 0, 5};
 
 // Rotation parameters of one slot pair.  Padded to 48 bytes (DOA_EIG_PRMPAD) so the eight pairs'
 // 16-byte halves fall in distinct shared-memory banks: phase 2b's loads (pairs k and k+4 in one
