@@ -38,6 +38,9 @@ namespace {
 constexpr int kN = 16;            // padded order
 constexpr int kLd = 17;           // smem row stride (double2)
 constexpr int kEigWarps = 4;
+#ifndef DOA_EIG_PARAM
+#define DOA_EIG_PARAM 1       // short-chain rotation parameters (see phase 1)
+#endif
 #ifndef DOA_EIG_MINB
 #define DOA_EIG_MINB 5
 #endif
@@ -210,6 +213,29 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
         }
         const double r2 = axy.x * axy.x + axy.y * axy.y;
         const bool rot = r2 > 1e-300;                         // a_xy ~ 0: identity rotation
+#if DOA_EIG_PARAM
+        // Short-chain parameters (same rotation as GvL sym.schur2): with d = (a_yy - a_xx)/2,
+        // r = |a_xy|, h = sqrt(d^2 + r^2), q = |d| + h:  t = sign(d) r / q,  c = sqrt(q / 2h),
+        // s = sign(d) r / sqrt(2 h q)  (c^2 + s^2 = 1 exactly in exact arithmetic), t r = sign(d) r^2 / q.
+        // c's critical path is two MUFU+Newton reciprocal square roots instead of four chained
+        // reciprocal (square) roots; s, e and t r run on parallel branches.
+        const double ir = rsqrt_pos(rot ? r2 : 1.0);          // 1/|a_xy|
+        const double rr = r2 * ir;                            // |a_xy|
+        const double d = 0.5 * (ayy - axx);
+        const double h2 = fma(d, d, r2);
+        const double irh = rsqrt_pos(rot ? h2 : 1.0);          // 1/h
+        const double h = h2 * irh;
+        const double q = fabs(d) + h;
+        const double u = 0.5 * q * irh;                       // c^2, in [1/2, 1]
+        const double sabs = rr * rsqrt_pos(2.0 * h * q);
+        const double trabs = r2 * rcp_pos(rot ? q : 1.0);
+        const double tr = rot ? (d < 0.0 ? -trabs : trabs) : 0.0;   // t |a_xy|
+        Prm p;
+        p.c = rot ? u * rsqrt_pos(u) : 1.0;
+        p.s = rot ? (d < 0.0 ? -sabs : sabs) : 0.0;
+        p.er = rot ? axy.x * ir : 1.0;
+        p.ei = rot ? -axy.y * ir : 0.0;
+#else
         const double ir = rsqrt_pos(rot ? r2 : 1.0);          // 1/|a_xy|
         const double rr = r2 * ir;                            // |a_xy|
         const double tau = (ayy - axx) * (0.5 * ir);
@@ -234,6 +260,7 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
         p.s = t * p.c;
         p.er = rot ? axy.x * ir : 1.0;
         p.ei = rot ? -axy.y * ir : 0.0;
+#endif
         if (lane < 8) {
           prm[warp][lane] = p;
 #if DOA_EIG_F32_ANGLE
@@ -244,8 +271,13 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
           // (min, max) of the permuted pair, conjugation of a real value is a no-op
           An[wxy] = make_double2(cs * (axx - ayy) + (cc - ss) * rr, 0.0);
 #else
+#if DOA_EIG_PARAM
+          An[wxx] = make_double2(axx - tr, 0.0);
+          An[wyy] = make_double2(ayy + tr, 0.0);
+#else
           An[wxx] = make_double2(axx - t * rr, 0.0);
           An[wyy] = make_double2(ayy + t * rr, 0.0);
+#endif
           An[wxy] = make_double2(0.0, 0.0);
 #endif
         }

@@ -20,6 +20,10 @@
 namespace doa {
 namespace {
 
+#ifndef DOA_EIG_PARAM
+#define DOA_EIG_PARAM 1       // short-chain rotation parameters (as eig16)
+#endif
+
 struct PrmN {
   double c, s, er, ei;
 };
@@ -187,7 +191,30 @@ __global__ void __launch_bounds__(EigN<N>::T, 1) eigN_kernel(const double2* __re
         const double2 axy = A[rxy];
         const double axx = A[rxx].x, ayy = A[ryy].x;
         const double r2 = axy.x * axy.x + axy.y * axy.y;
-        const bool rot = r2 > 1e-300;
+        const bool rot = r2 > 1e-300;                         // a_xy ~ 0: identity rotation
+#if DOA_EIG_PARAM
+        // Short-chain parameters (same rotation as GvL sym.schur2): with d = (a_yy - a_xx)/2,
+        // r = |a_xy|, h = sqrt(d^2 + r^2), q = |d| + h:  t = sign(d) r / q,  c = sqrt(q / 2h),
+        // s = sign(d) r / sqrt(2 h q)  (c^2 + s^2 = 1 exactly in exact arithmetic), t r = sign(d) r^2 / q.
+        // c's critical path is two MUFU+Newton reciprocal square roots instead of four chained
+        // reciprocal (square) roots; s, e and t r run on parallel branches.
+        const double ir = rsqrt_p(rot ? r2 : 1.0);          // 1/|a_xy|
+        const double rr = r2 * ir;                            // |a_xy|
+        const double d = 0.5 * (ayy - axx);
+        const double h2 = fma(d, d, r2);
+        const double irh = rsqrt_p(rot ? h2 : 1.0);          // 1/h
+        const double h = h2 * irh;
+        const double q = fabs(d) + h;
+        const double u = 0.5 * q * irh;                       // c^2, in [1/2, 1]
+        const double sabs = rr * rsqrt_p(2.0 * h * q);
+        const double trabs = r2 * rcp_p(rot ? q : 1.0);
+        const double tr = rot ? (d < 0.0 ? -trabs : trabs) : 0.0;   // t |a_xy|
+        PrmN p;
+        p.c = rot ? u * rsqrt_p(u) : 1.0;
+        p.s = rot ? (d < 0.0 ? -sabs : sabs) : 0.0;
+        p.er = rot ? axy.x * ir : 1.0;
+        p.ei = rot ? -axy.y * ir : 0.0;
+#else
         const double ir = rsqrt_p(rot ? r2 : 1.0);
         const double rr = r2 * ir;
         const double tau = (ayy - axx) * (0.5 * ir);
@@ -201,10 +228,16 @@ __global__ void __launch_bounds__(EigN<N>::T, 1) eigN_kernel(const double2* __re
         p.s = t * p.c;
         p.er = rot ? axy.x * ir : 1.0;
         p.ei = rot ? -axy.y * ir : 0.0;
+#endif
         prm_cs[prm_slot<N>(tid)] = make_double2(p.c, p.s);
         prm_ee[prm_slot<N>(tid)] = make_double2(p.er, p.ei);
+#if DOA_EIG_PARAM
+        An[wxx] = make_double2(axx - tr, 0.0);
+        An[wyy] = make_double2(ayy + tr, 0.0);
+#else
         An[wxx] = make_double2(axx - t * rr, 0.0);
         An[wyy] = make_double2(ayy + t * rr, 0.0);
+#endif
         An[wxy] = make_double2(0.0, 0.0);
       }
       __syncthreads();
