@@ -155,6 +155,24 @@ doa_status_t doa_run_host(const doa_plan_t* plans, int32_t nplans, const float* 
                           int64_t N, int32_t* idx_host, float* val_host, int32_t* npk_host,
                           int32_t* info_host, doa_stream_t stream);
 
+/* On-device synthetic snapshots of the signal model Eq. 1:
+ * X = A(theta) S + W for the ULA a_m(theta) = exp(-j*pi*m*u), u = 2*(d/lambda)*sin(theta) (Q6), with
+ * D uncorrelated unit-power CN(0,1) sources and CN(0, sigma^2) noise, sigma^2 = 10^(-snr_db/10)
+ * (Q13, Q14).  Randomness is counter-based (Philox4x32-10, key = seed): sample k of snapshot n of
+ * frame f (k < D: source k, else the noise of element k - D) comes from counter (k/2, n, f_lo,
+ * f_hi) and Box-Muller in fp64, so every frame is reproducible on its own and independent of B,
+ * frame0 and the launch configuration (synth/philox.py is the same generator in numpy).
+ *  theta_deg  DEVICE double, [D] (theta_per_frame = 0: same DOAs for every frame) or [B][D]
+ *             (theta_per_frame = 1), degrees from broadside.
+ *  frame0     global index of the first frame (frames frame0 .. frame0+B-1 are generated).
+ *  X          DEVICE complex64 [B][N][M] (output, overwritten).
+ * Errors: M < 1, M > 64, D < 1, D > 63, N < 1, N > 2^24, B >= 2^31, d_over_lambda <= 0, non-finite snr_db, NULL or
+ * misaligned pointers -> DOA_ERR_INVALID_ARG (nothing enqueued).  Asynchronous on `stream`.
+ * Test-input machinery, not part of the estimator: the hot path never calls it. */
+doa_status_t doa_generate(int32_t M, double d_over_lambda, int32_t D, const double* theta_deg,
+                          int32_t theta_per_frame, double snr_db, uint64_t seed, int64_t frame0,
+                          int64_t B, int64_t N, float* X, doa_stream_t stream);
+
 /* Kernel launches the most recent call on this thread enqueued (for launch accounting). */
 int32_t doa_last_launch_count(void);
 

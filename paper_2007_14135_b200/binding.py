@@ -18,7 +18,7 @@ INFO_NOCONV, INFO_DEGENERATE, INFO_CAND_OVERFLOW, INFO_UNDERDETERMINED = 1, 2, 4
 STATUS = {0: "DOA_OK", 1: "DOA_ERR_INVALID_ARG", 2: "DOA_ERR_UNSUPPORTED", 3: "DOA_ERR_OUT_OF_MEMORY",
           4: "DOA_ERR_CUDA"}
 
-EXPORTS = ("doa_plan_create", "doa_plan_create_array", "doa_plan_destroy", "doa_plan_capacity", "doa_covariance", "doa_eig",
+EXPORTS = ("doa_generate", "doa_plan_create", "doa_plan_create_array", "doa_plan_destroy", "doa_plan_capacity", "doa_covariance", "doa_eig",
            "doa_spectrum", "doa_peaks", "doa_run", "doa_run_host", "doa_last_launch_count",
            "doa_status_string", "doa_last_error", "doa_version")
 
@@ -46,6 +46,7 @@ def _load():
     L.doa_peaks.argtypes = [vp, i64, i32p, fp, i32p, i32p, vp]
     L.doa_run.argtypes = [vp, fp, i64, i64, i32p, fp, i32p, fp, i32p, vp]
     L.doa_run_host.argtypes = [C.POINTER(C.c_void_p), i32, fp, i64, i64, i32p, fp, i32p, i32p, vp]
+    L.doa_generate.argtypes = [i32, d, i32, dp, i32, d, C.c_uint64, i64, i64, i64, fp, vp]
     L.doa_last_launch_count.restype = i32
     L.doa_status_string.argtypes = [C.c_int]
     L.doa_status_string.restype = C.c_char_p
@@ -114,6 +115,15 @@ def doa_plan_create_array(M, positions, D, az0_deg, daz_deg, naz, el0_deg, del_d
     _check(lib.doa_plan_create_array(C.byref(h), M, pos.ctypes.data_as(C.POINTER(C.c_double)), D, az0_deg, daz_deg,
                                      naz, el0_deg, del_deg, nel, int(bool(az_wrap)), a, max_batch))
     return h
+
+
+def doa_generate(M, d_over_lambda, D, theta_deg, snr_db, seed, frame0, X, stream=None):
+    """On-device Eq. 1 snapshots (NEXT-3).  theta_deg: float64 CUDA tensor (D,) or (B, D);
+    X: complex64 CUDA tensor (B, N, M), overwritten."""
+    B, N = X.shape[0], X.shape[1]
+    per_frame = 1 if theta_deg.dim() == 2 else 0
+    _check(lib.doa_generate(M, d_over_lambda, D, _ptr(theta_deg), per_frame, snr_db, int(seed), frame0, B, N,
+                            _ptr(_f32(X)), _stream(stream)))
 
 
 def doa_plan_destroy(plan):

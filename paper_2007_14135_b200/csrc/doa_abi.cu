@@ -87,6 +87,26 @@ void count_launch() { ++g_launches; }
 extern "C" {
 
 int32_t doa_version(void) { return 1; }
+
+doa_status_t doa_generate(int32_t M, double d_over_lambda, int32_t D, const double* theta_deg,
+                          int32_t theta_per_frame, double snr_db, uint64_t seed, int64_t frame0, int64_t B,
+                          int64_t N, float* X, doa_stream_t stream) {
+  g_launches = 0;
+  if (M < 1 || M > doa::kMaxM) return fail(DOA_ERR_INVALID_ARG, "doa_generate: M=%d outside [1, %d]", M, doa::kMaxM);
+  if (D < 1 || D > 63) return fail(DOA_ERR_INVALID_ARG, "doa_generate: D=%d outside [1, 63]", D);
+  if (N < 1 || N > ((int64_t)1 << 24)) return fail(DOA_ERR_INVALID_ARG, "doa_generate: N=%lld outside [1, 2^24]", (long long)N);
+  if (B >= ((int64_t)1 << 31)) return fail(DOA_ERR_INVALID_ARG, "doa_generate: B=%lld >= 2^31", (long long)B);
+  if (B < 0 || frame0 < 0) return fail(DOA_ERR_INVALID_ARG, "doa_generate: negative B or frame0");
+  if (!(d_over_lambda > 0.0) || !std::isfinite(d_over_lambda) || !std::isfinite(snr_db))
+    return fail(DOA_ERR_INVALID_ARG, "doa_generate: d/lambda must be positive and snr_db finite");
+  if (B == 0) return DOA_OK;
+  DOA_CHECK_PTR(theta_deg, 8);
+  DOA_CHECK_PTR(X, 8);
+  DOA_TRY(doa::launch_generate(M, d_over_lambda, D, theta_deg, theta_per_frame ? 1 : 0, snr_db, seed, frame0, B, N, X,
+                               reinterpret_cast<cudaStream_t>(stream)),
+          "doa_generate");
+  return DOA_OK;
+}
 int32_t doa_last_launch_count(void) { return g_launches; }
 const char* doa_last_error(void) { return g_err.c_str(); }
 

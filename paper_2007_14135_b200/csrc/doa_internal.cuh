@@ -86,6 +86,10 @@ cudaError_t launch_array_spectrum(const doa_plan_s* p, const double* lam, const 
 __host__ __device__ constexpr int array_terms(int M) { return 1 + M * (M - 1); }   // c_0 + (Re, Im) per pair
 __host__ __device__ constexpr int array_ksteps(int M) { return (array_terms(M) + 3) / 4; }
 
+// NEXT-3: on-device Eq. 1 snapshots (csrc/generate.cu)
+cudaError_t launch_generate(int M, double dl, int D, const double* theta, int per_frame, double snr_db, uint64_t seed,
+                            int64_t frame0, int64_t B, int64_t N, float* X, cudaStream_t s);
+
 void count_launch();
 
 }  // namespace doa
