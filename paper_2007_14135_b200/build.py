@@ -39,6 +39,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     objdir = tmp + ".objs"
     os.makedirs(objdir, exist_ok=True)
     comp = [f for f in FLAGS if f not in ("-shared", "-cudart", "static")]
+    comp += os.environ.get("DOA_NVCC_EXTRA", "").split()      # tuning builds only (A/B variants)
     defs = [f"-D{d}" for d in defines]
 
     def one(src):
