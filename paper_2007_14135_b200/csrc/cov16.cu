@@ -26,23 +26,16 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 __device__ constexpr int kTI[10] = {0, 0, 1, 2, 2, 3, 0, 0, 1, 1};
 __device__ constexpr int kTJ[10] = {0, 1, 1, 2, 3, 3, 2, 3, 2, 3};
 
-__global__ void __launch_bounds__(kCovWarps * 32) cov16_kernel(const float2* __restrict__ X, int64_t B, int64_t N,
-                                                             int M, double2* __restrict__ R) {
-  __shared__ double Gs[kCovWarps][32 * kGld];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t b = (int64_t)blockIdx.x * kCovWarps + warp;
-  if (b >= B) return;
+// The ten upper Gram tiles over snapshots [n_begin, n_end) (n_begin a multiple of 4), one warp.
+__device__ __forceinline__ void gram_tiles(const float2* __restrict__ Xb, int64_t n_begin, int64_t n_end, int M,
+                                           int lane, double (&acc)[10][2]) {
   const int r = lane >> 2, q = lane & 3;
-  const float2* Xb = X + (size_t)b * N * M;
   const bool lo_ok = r < M, hi_ok = r + 8 < M;
-
-  double acc[10][2];
 #pragma unroll
   for (int t = 0; t < 10; ++t) { acc[t][0] = 0.0; acc[t][1] = 0.0; }
-
   constexpr int U = 8;                       // k-steps in flight per warp
-  int64_t n0 = 0;
-  for (; n0 + 4 * U <= N; n0 += 4 * U) {
+  int64_t n0 = n_begin;
+  for (; n0 + 4 * U <= n_end; n0 += 4 * U) {
     float2 x0[U], x1[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -57,10 +50,10 @@ __global__ void __launch_bounds__(kCovWarps * 32) cov16_kernel(const float2* __r
       for (int t = 0; t < 10; ++t) dmma(acc[t][0], acc[t][1], y[kTI[t]], y[kTJ[t]]);
     }
   }
-  for (; n0 < N; n0 += 4) {                  // ragged tail (N not a multiple of 32)
+  for (; n0 < n_end; n0 += 4) {              // ragged tail
     const int64_t n = n0 + q;
     float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
-    if (n < N) {
+    if (n < n_end) {
       const float2* row = Xb + (size_t)n * M;
       if (lo_ok) a0 = __ldg(row + r);
       if (hi_ok) a1 = __ldg(row + r + 8);
@@ -69,9 +62,12 @@ __global__ void __launch_bounds__(kCovWarps * 32) cov16_kernel(const float2* __r
 #pragma unroll
     for (int t = 0; t < 10; ++t) dmma(acc[t][0], acc[t][1], y[kTI[t]], y[kTJ[t]]);
   }
+}
 
-  // D fragment of tile (I, J): lane holds G[8I + r][8J + 2q + e]; store G and its mirror
-  double* G = Gs[warp];
+// Gram tiles -> mirrored smem Gram G -> Hermitian R (/N, exact conjugate mirror, real diagonal)
+__device__ __forceinline__ void gram_to_r(const double (&acc)[10][2], double* G, int lane, int64_t N, int M,
+                                          double2* __restrict__ Rb) {
+  const int r = lane >> 2, q = lane & 3;
 #pragma unroll
   for (int t = 0; t < 10; ++t) {
 #pragma unroll
@@ -83,7 +79,6 @@ __global__ void __launch_bounds__(kCovWarps * 32) cov16_kernel(const float2* __r
   }
   __syncwarp();
   const double dn = (double)N;
-  double2* Rb = R + (size_t)b * M * M;
   for (int e = lane; e < M * M; e += 32) {
     const int i = e / M, j = e - (e / M) * M;
     if (i > j) continue;
@@ -95,10 +90,64 @@ __global__ void __launch_bounds__(kCovWarps * 32) cov16_kernel(const float2* __r
   }
 }
 
+__global__ void __launch_bounds__(kCovWarps * 32) cov16_kernel(const float2* __restrict__ X, int64_t B, int64_t N,
+                                                             int M, double2* __restrict__ R) {
+  __shared__ double Gs[kCovWarps][32 * kGld];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t b = (int64_t)blockIdx.x * kCovWarps + warp;
+  if (b >= B) return;
+  const float2* Xb = X + (size_t)b * N * M;
+  double acc[10][2];
+  gram_tiles(Xb, 0, N, M, lane, acc);
+
+  gram_to_r(acc, Gs[warp], lane, N, M, R + (size_t)b * M * M);
+}
+
+
+// Split-N variant for long frames (N > 256): a CTA of SW = min(8, ceil(N/128)) warps per frame,
+// warp w accumulating the snapshots [w Nw, (w+1) Nw) (Nw a multiple of 4); the partial tiles are
+// summed in warp order through shared memory (fixed order: deterministic, and the split depends
+// only on N, so a frame's R does not depend on the batch).  Cuts the single-frame latency of
+// C2/C3 (N = 1024) roughly by SW.
+constexpr int kSplitMax = 8;
+__global__ void __launch_bounds__(kSplitMax * 32) cov16_split_kernel(const float2* __restrict__ X, int64_t N, int M,
+                                                                    int SW, double2* __restrict__ R) {
+  __shared__ double part[kSplitMax][10][64];      // the reduced Gram G reuses it afterwards
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t b = blockIdx.x;
+  const float2* Xb = X + (size_t)b * N * M;
+  const int64_t Nw = ((N + SW - 1) / SW + 3) / 4 * 4;
+  const int64_t n_begin = warp * Nw, n_end = n_begin + Nw < N ? n_begin + Nw : N;
+  double acc[10][2];
+  gram_tiles(Xb, n_begin < N ? n_begin : N, n_end > n_begin ? n_end : n_begin, M, lane, acc);
+#pragma unroll
+  for (int t = 0; t < 10; ++t) {
+    part[warp][t][2 * lane] = acc[t][0];
+    part[warp][t][2 * lane + 1] = acc[t][1];
+  }
+  __syncthreads();
+  if (warp != 0) return;
+#pragma unroll
+  for (int t = 0; t < 10; ++t) {
+    double s0 = part[0][t][2 * lane], s1 = part[0][t][2 * lane + 1];
+    for (int w = 1; w < SW; ++w) { s0 += part[w][t][2 * lane]; s1 += part[w][t][2 * lane + 1]; }
+    acc[t][0] = s0;
+    acc[t][1] = s1;
+  }
+  __syncwarp();
+  gram_to_r(acc, &part[0][0][0], lane, N, M, R + (size_t)b * M * M);
+}
+
 }  // namespace
 
 cudaError_t launch_cov16(const float* X, int64_t B, int64_t N, int M, double* R, cudaStream_t s) {
   count_launch();
+  if (N > 256) {
+    const int SW = (int)((N + 127) / 128 < kSplitMax ? (N + 127) / 128 : kSplitMax);
+    cov16_split_kernel<<<(unsigned)B, SW * 32, 0, s>>>(reinterpret_cast<const float2*>(X), N, M, SW,
+                                                       reinterpret_cast<double2*>(R));
+    return cudaGetLastError();
+  }
   cov16_kernel<<<(unsigned)((B + kCovWarps - 1) / kCovWarps), kCovWarps * 32, 0, s>>>(
       reinterpret_cast<const float2*>(X), B, N, M, reinterpret_cast<double2*>(R));
   return cudaGetLastError();
