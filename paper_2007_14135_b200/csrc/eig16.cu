@@ -178,7 +178,9 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
 
   int flag = 0;
   int cur = 0;
+  int nsw = 0;
   for (int sweep = 0;; ++sweep) {
+    nsw = sweep;
     {
       const double2* A = As[warp][cur];
       double off = 0.0;
@@ -351,6 +353,9 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
       if (j < M) Vrow[rank_s[warp][j]] = v[k];
     }
   }
+#ifdef DOA_EIG_COUNT
+  flag |= nsw << 8;                                      // diagnostic builds only: sweeps in bits 8+
+#endif
   if (lane == 0) info[b] = flag;
 }
 
