@@ -91,3 +91,22 @@ def test_plan_create_array_validation(lib, M, D, naz, nel, daz, dele, status):
     st = lib.lib.doa_plan_create_array(C.byref(h), M, pos.ctypes.data_as(C.POINTER(C.c_double)), D, 0.0, daz,
                                        naz, 90.0, dele, nel, 1, 1, 1)
     assert st == status and h.value is None
+
+
+@pytest.mark.parametrize("M,dl,D,snr,N,B,ok", [
+    (0, 0.5, 1, 10.0, 8, 1, False),            # M < 1
+    (65, 0.5, 1, 10.0, 8, 1, False),           # M > 64
+    (8, 0.5, 0, 10.0, 8, 1, False),            # D < 1
+    (8, 0.5, 64, 10.0, 8, 1, False),           # D > 63
+    (8, 0.0, 2, 10.0, 8, 1, False),            # d/lambda <= 0
+    (8, 0.5, 2, float("nan"), 8, 1, False),    # non-finite SNR
+    (8, 0.5, 2, 10.0, 0, 1, False),            # N < 1
+    (8, 0.5, 2, 10.0, 8, -1, False),           # B < 0
+    (8, 0.5, 2, 10.0, 8, 0, True),             # B == 0: nothing to do, OK
+])
+def test_generate_validation(lib, M, dl, D, snr, N, B, ok):
+    """doa_generate validates before touching the device (NULL pointers are fine for B == 0)."""
+    st = lib.lib.doa_generate(M, dl, D, None, 0, snr, 1, 0, B, N, None, None)
+    assert (st == 0) == ok
+    if not ok:
+        assert st == 1 and len(lib.lib.doa_last_error()) > 0
