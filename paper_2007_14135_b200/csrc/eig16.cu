@@ -41,6 +41,9 @@ constexpr int kEigWarps = 4;
 #ifndef DOA_EIG_PARAM
 #define DOA_EIG_PARAM 1       // short-chain rotation parameters (see phase 1)
 #endif
+#ifndef DOA_EIG_HALF
+#define DOA_EIG_HALF 1        // two matrices per warp, one per half (eig16h_kernel)
+#endif
 #ifndef DOA_EIG_MINB
 #define DOA_EIG_MINB 5
 #endif
@@ -359,10 +362,211 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
   if (lane == 0) info[b] = flag;
 }
 
+// Half-warp variant (DOA_EIG_HALF): two matrices per warp, one per 16-lane half.  Phase 1 of both
+// matrices runs in the same instructions (lanes 0-7 and 16-23), so the redundant rotation lanes
+// drop from 24 to 16 per matrix; each lane of a half owns one full row of V (16 complex) and two
+// of the 28 off-diagonal blocks.  A converged matrix keeps running with identity rotations
+// (c = 1, s = 0, e = 1: exact copies), so its outputs equal the one-matrix kernel's whatever
+// its partner needs.
+constexpr int kHWarps = 2;
+#ifndef DOA_EIGH_MINB
+#define DOA_EIGH_MINB 6
+#endif
+__device__ __forceinline__ double flipb(double x, int bit) {      // conjugate when bit set
+  return __longlong_as_double(__double_as_longlong(x) ^ ((long long)bit << 63));
+}
+__device__ __forceinline__ double hsum(double v) {               // sum over a 16-lane half
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ constexpr int kCatNext[16] = {0, 2, 4, 1, 6, 3, 8, 5, 10, 7, 12, 9, 14, 11, 15, 13};
+
+__global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(const double2* __restrict__ R,
+                                                                             int64_t B, int M,
+                                                                             double* __restrict__ lam_out,
+                                                                             double2* __restrict__ V_out,
+                                                                             int32_t* __restrict__ info) {
+  __shared__ double2 As[kHWarps][2][2][kN * kLd];          // [warp][half][buffer]
+  __shared__ Prm prm[kHWarps][2][kN / 2];
+  __shared__ int rank_s[kHWarps][2][kN];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int hm = lane >> 4, hl = lane & 15;
+  const int64_t b = ((int64_t)blockIdx.x * kHWarps + warp) * 2 + hm;
+  const bool valid = b < B;
+  Prm* pm = prm[warp][hm];
+
+  double nrm = 0.0;
+  {
+    const double2* Rb = R + (size_t)(valid ? b : 0) * M * M;
+    for (int e = hl; e < kN * kN; e += 16) {
+      const int i = e >> 4, j = e & 15;
+      if (i > j) continue;
+      double2 v = make_double2(0.0, 0.0);
+      if (valid && j < M) v = Rb[(size_t)i * M + j];
+      if (i == j) v.y = 0.0;
+      As[warp][hm][0][aidx(i, j)] = v;
+      nrm += (i == j ? 1.0 : 2.0) * (v.x * v.x + v.y * v.y);
+    }
+  }
+  const double tol = 10.0 * DBL_EPSILON * sqrt(hsum(nrm));
+
+  double2 v[16];                                           // row hl of this half's V
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = make_double2(k == hl ? 1.0 : 0.0, 0.0);
+
+  // two off-diagonal blocks per lane: t = hl and hl + 16 (< 28), row-major (r < s) order
+  int rb2[2], sb2[2], rd[2][4], wr[2][4], sgm[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    int l = hl + 16 * u;
+    if (l >= 28) l = 0;
+    int rb = 0, sb = 1;
+    for (int r = 0; r < 8; ++r) {
+      const int cntr = 7 - r;
+      if (l < cntr) { rb = r; sb = r + 1 + l; break; }
+      l -= cntr;
+    }
+    rb2[u] = rb; sb2[u] = sb;
+    const int i0 = 2 * rb, i1 = i0 + 1, j0 = 2 * sb, j1 = j0 + 1;
+    rd[u][0] = aidx(i0, j0); rd[u][1] = aidx(i0, j1); rd[u][2] = aidx(i1, j0); rd[u][3] = aidx(i1, j1);
+    const int pr[2] = {cat_next(i0), cat_next(i1)}, pc[2] = {cat_next(j0), cat_next(j1)};
+    int m = 0;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int x = pr[a], y = pc[c];
+        wr[u][2 * a + c] = x < y ? aidx(x, y) : aidx(y, x);
+        m |= (x < y ? 0 : 1) << (2 * a + c);
+      }
+    sgm[u] = m;
+  }
+  const bool has2 = hl + 16 < 28;
+  const int kx = 2 * (hl & 7), ky = kx + 1, px = cat_next(kx), py = cat_next(ky);
+  const int rxy = aidx(kx, ky), rxx = aidx(kx, kx), ryy = aidx(ky, ky);
+  const int wxx = aidx(px, px), wyy = aidx(py, py), wxy = px < py ? aidx(px, py) : aidx(py, px);
+  __syncwarp();
+
+  int flag = 0;
+  int cur = 0;
+  bool act = valid;
+  for (int sweep = 0;; ++sweep) {
+    {
+      const double2* A = As[warp][hm][cur];
+      double off = 0.0;
+      for (int e = hl; e < kN * kN; e += 16) {
+        const int i = e >> 4, j = e & 15;
+        if (i < j) { const double2 a = A[aidx(i, j)]; off += a.x * a.x + a.y * a.y; }
+      }
+      off = sqrt(2.0 * hsum(off));
+      if (act && off <= tol) act = false;
+      else if (act && sweep == kMaxSweeps) { flag |= DOA_INFO_NOCONV; act = false; }
+    }
+    if (!__any_sync(0xffffffffu, act)) break;
+#pragma unroll 1
+    for (int rnd = 0; rnd < kN - 1; ++rnd) {
+      const double2* A = As[warp][hm][cur];
+      double2* An = As[warp][hm][cur ^ 1];
+      {
+        double2 axy = make_double2(1.0, 0.0);
+        double axx = 0.0, ayy = 0.0;
+        if (hl < 8) {
+          axy = A[rxy];
+          axx = A[rxx].x;
+          ayy = A[ryy].x;
+        }
+        const double r2 = axy.x * axy.x + axy.y * axy.y;
+        const bool rot = act && r2 > 1e-300;               // frozen matrices: identity rotations
+        const double ir = rsqrt_pos(rot ? r2 : 1.0);
+        const double rr = r2 * ir;
+        const double d = 0.5 * (ayy - axx);
+        const double h2 = fma(d, d, r2);
+        const double irh = rsqrt_pos(rot ? h2 : 1.0);
+        const double hh = h2 * irh;
+        const double q = fabs(d) + hh;
+        const double uu = 0.5 * q * irh;
+        const double sabs = rr * rsqrt_pos(2.0 * hh * q);
+        const double trabs = r2 * rcp_pos(rot ? q : 1.0);
+        const double tr = rot ? (d < 0.0 ? -trabs : trabs) : 0.0;
+        Prm p;
+        p.c = rot ? uu * rsqrt_pos(uu) : 1.0;
+        p.s = rot ? (d < 0.0 ? -sabs : sabs) : 0.0;
+        p.er = rot ? axy.x * ir : 1.0;
+        p.ei = rot ? -axy.y * ir : 0.0;
+        if (hl < 8) {
+          pm[hl] = p;
+          An[wxx] = make_double2(axx - tr, 0.0);
+          An[wyy] = make_double2(ayy + tr, 0.0);
+          An[wxy] = act ? make_double2(0.0, 0.0) : A[rxy];   // frozen: keep the element as it is
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (u == 1 && !has2) break;
+        const Prm pr = pm[rb2[u]], ps = pm[sb2[u]];
+        const double2 b00 = A[rd[u][0]], b01 = A[rd[u][1]], b10 = A[rd[u][2]], b11 = A[rd[u][3]];
+        const double2 es = make_double2(ps.er, ps.ei), er = make_double2(pr.er, pr.ei);
+        const double2 t0 = cmul(es, b01), t1 = cmul(es, b11);
+        const double2 n00 = make_double2(ps.c * b00.x - ps.s * t0.x, ps.c * b00.y - ps.s * t0.y);
+        const double2 n01 = make_double2(ps.s * b00.x + ps.c * t0.x, ps.s * b00.y + ps.c * t0.y);
+        const double2 n10 = make_double2(ps.c * b10.x - ps.s * t1.x, ps.c * b10.y - ps.s * t1.y);
+        const double2 n11 = make_double2(ps.s * b10.x + ps.c * t1.x, ps.s * b10.y + ps.c * t1.y);
+        const double2 u0 = cmulc(er, n10), u1 = cmulc(er, n11);
+        const int m = sgm[u];
+        An[wr[u][0]] = make_double2(pr.c * n00.x - pr.s * u0.x, flipb(pr.c * n00.y - pr.s * u0.y, m & 1));
+        An[wr[u][1]] = make_double2(pr.c * n01.x - pr.s * u1.x, flipb(pr.c * n01.y - pr.s * u1.y, (m >> 1) & 1));
+        An[wr[u][2]] = make_double2(pr.s * n00.x + pr.c * u0.x, flipb(pr.s * n00.y + pr.c * u0.y, (m >> 2) & 1));
+        An[wr[u][3]] = make_double2(pr.s * n01.x + pr.c * u1.x, flipb(pr.s * n01.y + pr.c * u1.y, (m >> 3) & 1));
+      }
+      // V <- V J on the lane's row, then the slot permutation (register renaming + moves)
+      double2 t[16];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const Prm p = pm[k];
+        const double2 vx = v[2 * k], vy = v[2 * k + 1];
+        const double2 ey = cmul(make_double2(p.er, p.ei), vy);
+        t[kCatNext[2 * k]] = make_double2(p.c * vx.x - p.s * ey.x, p.c * vx.y - p.s * ey.y);
+        t[kCatNext[2 * k + 1]] = make_double2(p.s * vx.x + p.c * ey.x, p.s * vx.y + p.c * ey.y);
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = t[k];
+      cur ^= 1;
+      __syncwarp();
+    }
+  }
+
+  const double2* A = As[warp][hm][cur];
+  if (hl < M) {
+    const double li = A[aidx(hl, hl)].x;
+    int rk = 0;
+    for (int j = 0; j < M; ++j) {
+      const double lj = A[aidx(j, j)].x;
+      rk += (lj < li) || (lj == li && j < hl);
+    }
+    rank_s[warp][hm][hl] = rk;
+    if (valid) lam_out[(size_t)b * M + rk] = li;
+  }
+  __syncwarp();
+  if (valid && hl < M) {
+    double2* Vrow = V_out + (size_t)b * M * M + (size_t)hl * M;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k < M) Vrow[rank_s[warp][hm][k]] = v[k];
+  }
+  if (valid && hl == 0) info[b] = flag;
+}
+
 }  // namespace
 
 cudaError_t launch_eig16(const double* R, int64_t B, int M, double* lam, double* V, int32_t* info, cudaStream_t s) {
   count_launch();
+  if (DOA_EIG_HALF) {
+    eig16h_kernel<<<(unsigned)((B + 2 * kHWarps - 1) / (2 * kHWarps)), kHWarps * 32, 0, s>>>(
+        reinterpret_cast<const double2*>(R), B, M, lam, reinterpret_cast<double2*>(V), info);
+    return cudaGetLastError();
+  }
   eig16_kernel<<<(unsigned)((B + kEigWarps - 1) / kEigWarps), kEigWarps * 32, 0, s>>>(
       reinterpret_cast<const double2*>(R), B, M, lam, reinterpret_cast<double2*>(V), info);
   return cudaGetLastError();
