@@ -381,6 +381,11 @@ __device__ __forceinline__ double hsum(double v) {               // sum over a 1
   return v;
 }
 __device__ constexpr int kCatNext[16] = {0, 2, 4, 1, 6, 3, 8, 5, 10, 7, 12, 9, 14, 11, 15, 13};
+// half-lane -> block (row-major r < s index): pass 1 lanes 0-15 take entries 0-15, pass 2 lanes
+// 0-11 entries 16-27; from the quarter-warp bank-conflict search (48 wavefronts per round for
+// the block loads / permuted stores + phase 1, against 70 in natural order; ideal 38)
+__device__ constexpr int kHalfOrder[28] = {11, 8, 13, 5, 10, 4, 2, 25, 22, 0, 15, 23, 19, 20,
+                                           21, 18, 12, 7, 14, 27, 26, 9, 17, 16, 1, 3, 6, 24};
 
 __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(const double2* __restrict__ R,
                                                                              int64_t B, int M,
@@ -420,7 +425,7 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     int l = hl + 16 * u;
-    if (l >= 28) l = 0;
+    l = l < 28 ? kHalfOrder[l] : 0;
     int rb = 0, sb = 1;
     for (int r = 0; r < 8; ++r) {
       const int cntr = 7 - r;
