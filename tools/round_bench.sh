@@ -11,4 +11,4 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_r
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $OUT/launches_$TAG.csv \
    python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 python tools/launch_summary.py $OUT/launches_$TAG.csv > $OUT/launches_$TAG.txt; cat $OUT/launches_$TAG.txt
-bash tools/prof.sh $TAG scan_cta eig16 cov16 coef_mma select_kernel
+bash tools/prof.sh $TAG scan_cta eig16h cov16 coef_mma select_kernel
