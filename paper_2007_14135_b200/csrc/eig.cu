@@ -1,5 +1,6 @@
 // S2 dispatch — batched Hermitian eigendecomposition (Table 2 Step-2 `jsvd`; Q3):
-//   M <= 16        eig16_kernel (csrc/eig16.cu): one warp per matrix
+//   M <= 16        eig16h_kernel (csrc/eig16.cu): two matrices per warp, one per 16-lane half
+//                  (eig16_kernel, one warp per matrix, with DOA_EIG_HALF=0)
 //   16 < M <= 64   eigN_kernel<32|64> (csrc/eign.cu): one CTA per matrix
 // Both are the parallel (circle-method round robin) cyclic Jacobi with a fixed-slot caterpillar
 // permutation; see the kernel files.

@@ -6,8 +6,10 @@
 //     a^H C a = sum_{p,q} C_pq z^{q-p} = c_0 + 2 Re sum_{k>=1} c_k z^k,   c_k = sum_p C[p][p+k].
 // Each (frame, angle) then costs 2(M-1) fp64 FMAs against a per-angle table
 // T(psi) = (1, cos k psi, sin k psi) shared by every frame — the scan is the real contraction
-// F[b][i] = sum_j coef[b][j] T[j][i] (Table 2 Step-5), K = 4S >= 2M-1, run on the FP64
-// tensor pipe (DMMA, mma.sync m8n8k4 f64) with the table staged once per CTA in shared memory.
+// F[b][i] = sum_j coef[b][j] T[j][i] (Table 2 Step-5), K = 4S (even and odd halves, see
+// doa_internal.cuh), run on the FP64 tensor pipe (DMMA, mma.sync m8n8k4 f64) with the table
+// staged once per CTA in shared memory.  On symmetric grids (Q26) one contraction
+// yields a mirrored pair of angles (f = E + O and E - O).
 #include <cfloat>
 
 #include "doa_internal.cuh"
