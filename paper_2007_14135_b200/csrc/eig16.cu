@@ -1,4 +1,6 @@
-// S2 for M <= 16: batched Hermitian Jacobi eigendecomposition, one warp per matrix.
+// S2 for M <= 16: batched Hermitian Jacobi eigendecomposition — eig16_kernel (one warp per
+// matrix, described below) and eig16h_kernel (the default: the same rounds with two matrices per
+// warp, one per 16-lane half; see its comment further down).
 // (Table 2 Step-2 `jsvd`; read as the Hermitian eigendecomposition, Q3.)
 //
 // Ordering: parallel cyclic Jacobi with the circle-method round robin on n = 16 indices (M < 16
