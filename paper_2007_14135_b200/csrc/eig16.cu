@@ -43,6 +43,12 @@ constexpr int kEigWarps = 4;
 #ifndef DOA_EIG_PARAM
 #define DOA_EIG_PARAM 1       // short-chain rotation parameters (see phase 1)
 #endif
+#ifndef DOA_EIG_HALF_MIN_B
+#define DOA_EIG_HALF_MIN_B 2048  // below this batch size M > 8 uses eig16_kernel
+#endif
+#ifndef DOA_EIG_N8
+#define DOA_EIG_N8 1          // M <= 8: 8-index round robin (eig16h_kernel<8>)
+#endif
 #ifndef DOA_EIG_HALF
 #define DOA_EIG_HALF 1        // two matrices per warp, one per half (eig16h_kernel)
 #endif
@@ -382,21 +388,31 @@ __device__ __forceinline__ double hsum(double v) {               // sum over a 1
   for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-__device__ constexpr int kCatNext[16] = {0, 2, 4, 1, 6, 3, 8, 5, 10, 7, 12, 9, 14, 11, 15, 13};
 // half-lane -> block (row-major r < s index): pass 1 lanes 0-15 take entries 0-15, pass 2 lanes
 // 0-11 entries 16-27; from the quarter-warp bank-conflict search (48 wavefronts per round for
 // the block loads / permuted stores + phase 1, against 70 in natural order; ideal 38)
 __device__ constexpr int kHalfOrder[28] = {11, 8, 13, 5, 10, 4, 2, 25, 22, 0, 15, 23, 19, 20,
                                            21, 18, 12, 7, 14, 27, 26, 9, 17, 16, 1, 3, 6, 24};
 
+// N = 16 or 8 (M <= 8 uses the 8-index round robin: 7 rounds of 4 rotations per sweep).
+template <int N> struct HLd { static constexpr int LD = N == 16 ? kLd : 9; };
+template <int N>
+__device__ __forceinline__ int aidxT(int i, int j) { return i * HLd<N>::LD + (j ^ (i >> 1)); }
+__host__ __device__ constexpr int cat_next_c(int s, int n) {
+  return s == 0 ? 0 : (s == 1 ? 2 : (s == n - 2 ? n - 1 : ((s & 1) ? s - 2 : s + 2)));
+}
+template <int N>
+__device__ __forceinline__ int cat_nextT(int s) { return cat_next_c(s, N); }
+
+template <int N>
 __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(const double2* __restrict__ R,
                                                                              int64_t B, int M,
                                                                              double* __restrict__ lam_out,
                                                                              double2* __restrict__ V_out,
                                                                              int32_t* __restrict__ info) {
-  __shared__ double2 As[kHWarps][2][2][kN * kLd];          // [warp][half][buffer]
-  __shared__ Prm prm[kHWarps][2][kN / 2];
-  __shared__ int rank_s[kHWarps][2][kN];
+  __shared__ double2 As[kHWarps][2][2][N * HLd<N>::LD];          // [warp][half][buffer]
+  __shared__ Prm prm[kHWarps][2][N / 2];
+  __shared__ int rank_s[kHWarps][2][N];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int hm = lane >> 4, hl = lane & 15;
   const int64_t b = ((int64_t)blockIdx.x * kHWarps + warp) * 2 + hm;
@@ -406,53 +422,54 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
   double nrm = 0.0;
   {
     const double2* Rb = R + (size_t)(valid ? b : 0) * M * M;
-    for (int e = hl; e < kN * kN; e += 16) {
-      const int i = e >> 4, j = e & 15;
+    for (int e = hl; e < N * N; e += 16) {
+      const int i = e / N, j = e % N;
       if (i > j) continue;
       double2 v = make_double2(0.0, 0.0);
       if (valid && j < M) v = Rb[(size_t)i * M + j];
       if (i == j) v.y = 0.0;
-      As[warp][hm][0][aidx(i, j)] = v;
+      As[warp][hm][0][aidxT<N>(i, j)] = v;
       nrm += (i == j ? 1.0 : 2.0) * (v.x * v.x + v.y * v.y);
     }
   }
   const double tol = 10.0 * DBL_EPSILON * sqrt(hsum(nrm));
 
-  double2 v[16];                                           // row hl of this half's V
+  double2 v[N];                                           // row hl of this half's V
 #pragma unroll
-  for (int k = 0; k < 16; ++k) v[k] = make_double2(k == hl ? 1.0 : 0.0, 0.0);
+  for (int k = 0; k < N; ++k) v[k] = make_double2(k == hl ? 1.0 : 0.0, 0.0);
 
-  // two off-diagonal blocks per lane: t = hl and hl + 16 (< 28), row-major (r < s) order
-  int rb2[2], sb2[2], rd[2][4], wr[2][4], sgm[2];
+  // off-diagonal blocks per lane: t = hl (+ 16) < NBLK, row-major (r < s) order
+  constexpr int NP = N / 2, NBLK = NP * (NP - 1) / 2, BPL = (NBLK + 15) / 16;
+  int rb2[BPL], sb2[BPL], rd[BPL][4], wr[BPL][4], sgm[BPL];
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
+  for (int u = 0; u < BPL; ++u) {
     int l = hl + 16 * u;
-    l = l < 28 ? kHalfOrder[l] : 0;
+    l = l < NBLK ? (N == 16 ? kHalfOrder[l] : l) : 0;
     int rb = 0, sb = 1;
-    for (int r = 0; r < 8; ++r) {
-      const int cntr = 7 - r;
+    for (int r = 0; r < NP; ++r) {
+      const int cntr = NP - 1 - r;
       if (l < cntr) { rb = r; sb = r + 1 + l; break; }
       l -= cntr;
     }
     rb2[u] = rb; sb2[u] = sb;
     const int i0 = 2 * rb, i1 = i0 + 1, j0 = 2 * sb, j1 = j0 + 1;
-    rd[u][0] = aidx(i0, j0); rd[u][1] = aidx(i0, j1); rd[u][2] = aidx(i1, j0); rd[u][3] = aidx(i1, j1);
-    const int pr[2] = {cat_next(i0), cat_next(i1)}, pc[2] = {cat_next(j0), cat_next(j1)};
+    rd[u][0] = aidxT<N>(i0, j0); rd[u][1] = aidxT<N>(i0, j1); rd[u][2] = aidxT<N>(i1, j0); rd[u][3] = aidxT<N>(i1, j1);
+    const int pr[2] = {cat_nextT<N>(i0), cat_nextT<N>(i1)}, pc[2] = {cat_nextT<N>(j0), cat_nextT<N>(j1)};
     int m = 0;
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int x = pr[a], y = pc[c];
-        wr[u][2 * a + c] = x < y ? aidx(x, y) : aidx(y, x);
+        wr[u][2 * a + c] = x < y ? aidxT<N>(x, y) : aidxT<N>(y, x);
         m |= (x < y ? 0 : 1) << (2 * a + c);
       }
     sgm[u] = m;
   }
-  const bool has2 = hl + 16 < 28;
-  const int kx = 2 * (hl & 7), ky = kx + 1, px = cat_next(kx), py = cat_next(ky);
-  const int rxy = aidx(kx, ky), rxx = aidx(kx, kx), ryy = aidx(ky, ky);
-  const int wxx = aidx(px, px), wyy = aidx(py, py), wxy = px < py ? aidx(px, py) : aidx(py, px);
+  const bool has2 = hl + 16 < NBLK;
+  const int kx = 2 * (hl % NP), ky = kx + 1, px = cat_nextT<N>(kx), py = cat_nextT<N>(ky);
+  const int rxy = aidxT<N>(kx, ky), rxx = aidxT<N>(kx, kx), ryy = aidxT<N>(ky, ky);
+  const int wxx = aidxT<N>(px, px), wyy = aidxT<N>(py, py), wxy = px < py ? aidxT<N>(px, py) : aidxT<N>(py, px);
   __syncwarp();
 
   int flag = 0;
@@ -462,9 +479,9 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
     {
       const double2* A = As[warp][hm][cur];
       double off = 0.0;
-      for (int e = hl; e < kN * kN; e += 16) {
-        const int i = e >> 4, j = e & 15;
-        if (i < j) { const double2 a = A[aidx(i, j)]; off += a.x * a.x + a.y * a.y; }
+      for (int e = hl; e < N * N; e += 16) {
+        const int i = e / N, j = e % N;
+        if (i < j) { const double2 a = A[aidxT<N>(i, j)]; off += a.x * a.x + a.y * a.y; }
       }
       off = sqrt(2.0 * hsum(off));
       if (act && off <= tol) act = false;
@@ -472,13 +489,13 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
     }
     if (!__any_sync(0xffffffffu, act)) break;
 #pragma unroll 1
-    for (int rnd = 0; rnd < kN - 1; ++rnd) {
+    for (int rnd = 0; rnd < N - 1; ++rnd) {
       const double2* A = As[warp][hm][cur];
       double2* An = As[warp][hm][cur ^ 1];
       {
         double2 axy = make_double2(1.0, 0.0);
         double axx = 0.0, ayy = 0.0;
-        if (hl < 8) {
+        if (hl < NP) {
           axy = A[rxy];
           axx = A[rxx].x;
           ayy = A[ryy].x;
@@ -501,7 +518,7 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
         p.s = rot ? (d < 0.0 ? -sabs : sabs) : 0.0;
         p.er = rot ? axy.x * ir : 1.0;
         p.ei = rot ? -axy.y * ir : 0.0;
-        if (hl < 8) {
+        if (hl < NP) {
           pm[hl] = p;
           An[wxx] = make_double2(axx - tr, 0.0);
           An[wyy] = make_double2(ayy + tr, 0.0);
@@ -510,7 +527,7 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
       }
       __syncwarp();
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < BPL; ++u) {
         if (u == 1 && !has2) break;
         const Prm pr = pm[rb2[u]], ps = pm[sb2[u]];
         const double2 b00 = A[rd[u][0]], b01 = A[rd[u][1]], b10 = A[rd[u][2]], b11 = A[rd[u][3]];
@@ -528,17 +545,17 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
         An[wr[u][3]] = make_double2(pr.s * n01.x + pr.c * u1.x, flipb(pr.s * n01.y + pr.c * u1.y, (m >> 3) & 1));
       }
       // V <- V J on the lane's row, then the slot permutation (register renaming + moves)
-      double2 t[16];
+      double2 t[N];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < NP; ++k) {
         const Prm p = pm[k];
         const double2 vx = v[2 * k], vy = v[2 * k + 1];
         const double2 ey = cmul(make_double2(p.er, p.ei), vy);
-        t[kCatNext[2 * k]] = make_double2(p.c * vx.x - p.s * ey.x, p.c * vx.y - p.s * ey.y);
-        t[kCatNext[2 * k + 1]] = make_double2(p.s * vx.x + p.c * ey.x, p.s * vx.y + p.c * ey.y);
+        t[cat_next_c(2 * k, N)] = make_double2(p.c * vx.x - p.s * ey.x, p.c * vx.y - p.s * ey.y);
+        t[cat_next_c(2 * k + 1, N)] = make_double2(p.s * vx.x + p.c * ey.x, p.s * vx.y + p.c * ey.y);
       }
 #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = t[k];
+      for (int k = 0; k < N; ++k) v[k] = t[k];
       cur ^= 1;
       __syncwarp();
     }
@@ -546,10 +563,10 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
 
   const double2* A = As[warp][hm][cur];
   if (hl < M) {
-    const double li = A[aidx(hl, hl)].x;
+    const double li = A[aidxT<N>(hl, hl)].x;
     int rk = 0;
     for (int j = 0; j < M; ++j) {
-      const double lj = A[aidx(j, j)].x;
+      const double lj = A[aidxT<N>(j, j)].x;
       rk += (lj < li) || (lj == li && j < hl);
     }
     rank_s[warp][hm][hl] = rk;
@@ -559,7 +576,7 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
   if (valid && hl < M) {
     double2* Vrow = V_out + (size_t)b * M * M + (size_t)hl * M;
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
+    for (int k = 0; k < N; ++k)
       if (k < M) Vrow[rank_s[warp][hm][k]] = v[k];
   }
   if (valid && hl == 0) info[b] = flag;
@@ -569,9 +586,17 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
 
 cudaError_t launch_eig16(const double* R, int64_t B, int M, double* lam, double* V, int32_t* info, cudaStream_t s) {
   count_launch();
-  if (DOA_EIG_HALF) {
-    eig16h_kernel<<<(unsigned)((B + 2 * kHWarps - 1) / (2 * kHWarps)), kHWarps * 32, 0, s>>>(
-        reinterpret_cast<const double2*>(R), B, M, lam, reinterpret_cast<double2*>(V), info);
+  // small batches of M > 8 (latency-bound single frames) take the one-warp-per-matrix kernel,
+  // whose single-matrix round is shorter; it performs the same operations in the same order, so
+  // the results are bitwise the same (tests/test_gpu_parity.py::test_eig_kernels_bitwise_equal)
+  if (DOA_EIG_HALF && (M <= 8 || B >= DOA_EIG_HALF_MIN_B)) {
+    const unsigned g = (unsigned)((B + 2 * kHWarps - 1) / (2 * kHWarps));
+    if (M <= 8 && DOA_EIG_N8)
+      eig16h_kernel<8><<<g, kHWarps * 32, 0, s>>>(reinterpret_cast<const double2*>(R), B, M, lam,
+                                                   reinterpret_cast<double2*>(V), info);
+    else
+      eig16h_kernel<16><<<g, kHWarps * 32, 0, s>>>(reinterpret_cast<const double2*>(R), B, M, lam,
+                                                    reinterpret_cast<double2*>(V), info);
     return cudaGetLastError();
   }
   eig16_kernel<<<(unsigned)((B + kEigWarps - 1) / kEigWarps), kEigWarps * 32, 0, s>>>(

@@ -323,6 +323,19 @@ def test_randomized_sweep(doa, case):
         plan.close()
 
 
+def test_eig_kernels_bitwise_equal(doa):
+    """M = 16: small batches use the one-warp-per-matrix eigensolver, large ones the half-warp
+    kernel (two matrices per warp); a frame's eigenpairs must not depend on which ran."""
+    cfg = get_config("c4")
+    X = torch.from_numpy(generate(cfg, frames=range(4096))).cuda()
+    big = doa.Plan(cfg.M, cfg.D, "music", cfg.dtheta, max_batch=4096)
+    R = big.covariance(X)
+    lam_b, V_b, info_b = big.eig(R)
+    for b in (0, 1, 777, 4095):
+        lam_s, V_s, info_s = big.eig(R[b:b + 1].contiguous())
+        assert torch.equal(lam_s[0], lam_b[b]) and torch.equal(V_s[0], V_b[b]) and torch.equal(info_s[0], info_b[b])
+
+
 def test_determinism_and_batch_invariance(doa):
     cfg = get_config("c4")
     X = torch.from_numpy(generate(cfg, frames=range(300))).cuda()
