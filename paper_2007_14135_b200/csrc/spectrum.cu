@@ -230,13 +230,15 @@ __global__ void __launch_bounds__(kCoefMmaWarps * 32) coef_mma_kernel(const doub
   // EV weights w_j = 1/lambda_j (Q1), clamped at 100 eps lambda_max (DEGENERATE)
   double wj[4] = {1.0, 1.0, 1.0, 1.0};                 // weight of row j = 4J + lane%4 of X
   if (alg == DOA_ALG_EV) {
-    const double lfloor = 100.0 * DBL_EPSILON * fmax(lb[M - 1], 0.0);
-    for (int j = 0; j < K; ++j) if (lb[j] <= lfloor) flag |= DOA_INFO_DEGENERATE;
+    // lane j < K loads lambda_j once; weights and the DEGENERATE test are lane-parallel
+    const double lmax = lb[M - 1];
+    const double lfloor = 100.0 * DBL_EPSILON * fmax(lmax, 0.0);
+    const double lj = lane < K ? lb[lane] : 1.0;
+    const bool deg = lane < K && lj <= lfloor;
+    if (__any_sync(0xffffffffu, deg)) flag |= DOA_INFO_DEGENERATE;
+    const double w = lane < K ? (deg ? (lfloor > 0.0 ? 1.0 / lfloor : 1.0) : 1.0 / lj) : 0.0;
 #pragma unroll
-    for (int J = 0; J < 4; ++J) {
-      const int j = 4 * J + (lane & 3);
-      wj[J] = j < K ? (lb[j] <= lfloor ? (lfloor > 0.0 ? 1.0 / lfloor : 1.0) : 1.0 / lb[j]) : 0.0;
-    }
+    for (int J = 0; J < 4; ++J) wj[J] = __shfl_sync(0xffffffffu, w, 4 * J + (lane & 3));
   } else if (alg == DOA_ALG_MN) {
     // w = P_n e1 / (e1^H P_n e1): P_n e1 = sum_j e_j conj(e_j[0]), e1^H P_n e1 = sum_j |e_j[0]|^2
     double p0 = 0.0;
