@@ -241,8 +241,9 @@ __global__ void __launch_bounds__(kCoefMmaWarps * 32) coef_mma_kernel(const doub
     for (int J = 0; J < 4; ++J) wj[J] = __shfl_sync(0xffffffffu, w, 4 * J + (lane & 3));
   } else if (alg == DOA_ALG_MN) {
     // w = P_n e1 / (e1^H P_n e1): P_n e1 = sum_j e_j conj(e_j[0]), e1^H P_n e1 = sum_j |e_j[0]|^2
-    double p0 = 0.0;
-    for (int j = 0; j < K; ++j) p0 += Ure[j * ld] * Ure[j * ld] + Uim[j * ld] * Uim[j * ld];
+    double p0 = lane < K ? Ure[lane * ld] * Ure[lane * ld] + Uim[lane * ld] * Uim[lane * ld] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) p0 += __shfl_xor_sync(0xffffffffu, p0, o);   // fixed tree order
     const bool degen = !(p0 > 100.0 * DBL_EPSILON);
     if (degen) flag |= DOA_INFO_DEGENERATE;
     const double lp = degen ? 1.0 : 1.0 / p0;
@@ -389,8 +390,9 @@ __global__ void __launch_bounds__(kCoefBigWarps * 32) coef_big_kernel(const doub
   __syncthreads();
   int nv = (alg == DOA_ALG_MUSIC || alg == DOA_ALG_EV) ? K : 1;
   if (alg == DOA_ALG_MN) {
-    double p0 = 0.0;
-    for (int j = 0; j < K; ++j) p0 += Ure[j * ld] * Ure[j * ld] + Uim[j * ld] * Uim[j * ld];
+    double p0 = lane < K ? Ure[lane * ld] * Ure[lane * ld] + Uim[lane * ld] * Uim[lane * ld] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) p0 += __shfl_xor_sync(0xffffffffu, p0, o);   // fixed tree order
     const bool degen = !(p0 > 100.0 * DBL_EPSILON);
     const double lp = degen ? 1.0 : 1.0 / p0;
     double pr = 0.0, pi = 0.0;
