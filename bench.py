@@ -5,9 +5,12 @@
 One step = one batch of synthetic frames through the whole hot path for all four estimators:
 S1 covariance + S2 eigendecomposition once per frame, then S3-S7 (coefficients, scan, peaks) for
 PHD, MUSIC, EV and MN — all through the C ABI (include/doa.h) on device-resident inputs.  For
-N > 1 (torchrun) every rank owns its own batch of frames (weak scaling: frames are independent),
-and the per-frame peak lists are gathered to every rank with one NCCL all_gather per step (the
-only collective; north_star).  Rank 0 prints one JSON line.
+N > 1 (torchrun) the config's batch (c4: 65536 frames) is split into contiguous shards, one per
+rank (strong scaling, BASELINE configs[3]; `--scaling weak` gives every rank a full batch), and
+the per-frame peak lists are gathered to every rank in frame order with one NCCL all_gather per
+step (the only collective; north_star).  The compute part of the step is replayed as a CUDA graph;
+the gather runs after it.  The default c4 run also measures the north-star workload (c4's frames
+on the 0.001-degree grid) and reports it under "north_star".  Rank 0 prints one JSON line.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|ns|c2|...] [--impl ours|reference]
 """
@@ -40,7 +43,12 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
-                    help="replay the step as a CUDA graph (auto: single-GPU runs)")
+                    help="replay the compute part of the step as a CUDA graph (auto: on)")
+    ap.add_argument("--scaling", default="auto", choices=["auto", "strong", "weak"],
+                    help="strong (default for batched workloads): the config's batch is split across the GPUs; "
+                         "weak: every GPU owns a full batch")
+    ap.add_argument("--no-north-star", dest="north_star", action="store_false",
+                    help="skip the north-star (ns) measurement that the default c4 run adds")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle CPU time for cpu_baseline")
     return ap.parse_args()
 
@@ -168,8 +176,8 @@ def run_reference(args, cfg):
     v = n / dt
     line = {"metric": METRIC, "value": v, "unit": "frames/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(cfg, n, args.gpus),
+            "scaling": "strong" if cfg.B > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(cfg, n, args.gpus),
             "points_per_s": v * cfg.L * len(ALGS),
             "cpu_baseline": {"value": v, "unit": "frames/s", "cores": cores, "kind": "oracle",
                              "sample": f"{n} frames of {cfg.name} per step, all 4 algorithms, {cores} threads"},
@@ -191,6 +199,154 @@ def config_dict(cfg, frames_per_gpu, n_gpus):
 
 
 # ------------------------------------------------------------------------------------ our arm
+# Mean Jacobi sweeps of the M = 16 eigensolver on c4/ns frames (tools/eig_sweep_count.py, the
+# DOA_EIG_COUNT diagnostic build): the S2 term of the step roofline.
+EIG_SWEEPS_M16 = 7.72
+
+
+class Workload:
+    """Plans + buffers + the step of one ULA/array workload on this rank's frames."""
+
+    def __init__(self, cfg, is_array, X, B, dev, doa):
+        import torch
+        self.cfg, self.B, self.X = cfg, B, X
+        M, D = cfg.M, cfg.D
+        if is_array:
+            self.plans = [doa.Plan.array(cfg.pos, D, a, cfg.az0, cfg.daz, cfg.naz, cfg.el0, cfg.del_, cfg.nel,
+                                         cfg.az_wrap, max_batch=B, device=dev) for a in ALGS]
+        else:
+            self.plans = [doa.Plan(M, D, a, cfg.dtheta, L=cfg.L, theta0=cfg.theta0, d_over_lambda=cfg.d_over_lambda,
+                                   max_batch=B, device=dev) for a in ALGS]
+        self.R = torch.empty((B, M, M), dtype=torch.complex128, device=dev)
+        self.lam = torch.empty((B, M), dtype=torch.float64, device=dev)
+        self.V = torch.empty((B, M, M), dtype=torch.complex128, device=dev)
+        self.info_eig = torch.empty((B,), dtype=torch.int32, device=dev)
+        self.info = torch.empty((len(ALGS), B), dtype=torch.int32, device=dev)
+        self.idx = torch.empty((len(ALGS), B, D), dtype=torch.int32, device=dev)
+        self.val = torch.empty((len(ALGS), B, D), dtype=torch.float32, device=dev)
+        self.npk = torch.empty((len(ALGS), B), dtype=torch.int32, device=dev)
+        self.packed = torch.empty((len(ALGS), B, 2 * D + 2), dtype=torch.int32, device=dev)
+        self.spec_ev = []
+
+    def compute(self, sh, stream=None, record=False):
+        """S1-S7 for the four estimators on stream handle `sh` + packing of the peak lists;
+        returns the number of libdoa kernel launches."""
+        import torch
+        from paper_2007_14135_b200 import binding as bd
+        from paper_2007_14135_b200 import dist as pdist
+        n = 0
+        if self.B == 0:
+            return 0
+        bd.doa_covariance(self.plans[0].h, self.X, self.R, sh)
+        n += bd.doa_last_launch_count()
+        bd.doa_eig(self.plans[0].h, self.R, self.lam, self.V, self.info_eig, sh)
+        n += bd.doa_last_launch_count()
+        for a, p in enumerate(self.plans):
+            self.info[a].copy_(self.info_eig)
+            if record:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            bd.doa_spectrum(p.h, self.lam, self.V, self.info[a], None, sh)
+            n += bd.doa_last_launch_count()
+            if record:
+                e1.record(stream)
+                self.spec_ev.append((e0, e1))
+            bd.doa_peaks(p.h, self.B, self.idx[a], self.val[a], self.npk[a], self.info[a], sh)
+            n += bd.doa_last_launch_count()
+        pdist.pack_peaks(self.idx, self.val, self.npk, self.info, out=self.packed)
+        return n
+
+
+def timed_steps(args, wl, ws, dev, stream, use_graph, gather):
+    """Warm up, optionally capture the compute part of the step in a CUDA graph, then time exactly
+    args.steps steps between CUDA events on `stream` (barrier + synchronize on both sides) and take
+    the max over ranks.  gather() is the step's one collective (NCCL all_gather of the peak lists,
+    ws > 1), run eagerly after the replayed compute.  Returns (ms_per_step, launches, graph, clocks)."""
+    import torch
+    import torch.distributed as dist
+    s = stream.cuda_stream
+    for _ in range(max(3, args.warmup)):
+        wl.compute(s)
+        gather(wl)
+    torch.cuda.synchronize()
+    graph, per = None, 0
+    if use_graph:
+        for _ in range(min(args.steps, 5)):           # per-launch timing of doa_spectrum, outside the graph
+            wl.compute(s, stream, record=True)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            per = wl.compute(stream.cuda_stream)
+        for _ in range(max(3, args.warmup)):
+            graph.replay()
+            gather(wl)
+        torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    time.sleep(0.3)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    launches = 0
+    for _ in range(args.steps):
+        if graph is not None:
+            graph.replay()
+            launches += per
+        else:
+            launches += wl.compute(s, stream, record=True)
+        gather(wl)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    if ws > 1:
+        ms = max_over_ranks(ms, dev)
+        dist.barrier()
+    return ms / args.steps, launches, graph, clk
+
+
+def max_over_ranks(x: float, dev) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def scan_roofline(wl, is_array, mirrored):
+    """Roofline of the dominant kernel (the scan inside doa_spectrum) from its CUDA-event time."""
+    cfg = wl.cfg
+    M, L, B = cfg.M, cfg.L, wl.B
+    spec_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in wl.spec_ev)
+    if is_array:                                   # K - 1 = M(M-1) fp64 FMAs per (frame, grid point)
+        scan_flops = 2.0 * M * (M - 1) * L * B
+    elif mirrored:                                 # per mirrored pair: E and O (2(M-1) FMAs), E +- O (2 adds)
+        scan_flops = (2.0 * (M - 1) + 1.0) * L * B
+    else:                                          # 2(M-1) fp64 FMAs per (frame, angle)
+        scan_flops = 4.0 * (M - 1) * L * B
+    pk = peaks_json()
+    fp64_peak = 148 * 64 * 2 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12   # TFLOP/s, guide unit counts
+    achieved = scan_flops / (spec_ms / 1e3) / 1e12
+    return spec_ms, scan_flops, achieved, fp64_peak
+
+
+def step_roofline_ms(cfg, B, mirrored, fp64_peak_tflops):
+    """SURVEY §8(d) step roofline (T_roof = sum over stages of max(bytes/BW, flops/F64)) with the
+    scan's algorithmic work as the kernel does it (mirrored: 2(M-1)+1 flops per (frame, angle))."""
+    M, N, L = cfg.M, cfg.N, cfg.L
+    hbm = float(peaks_json().get("hbm_gbs", 6446.9)) * 1e9
+    f64 = fp64_peak_tflops * 1e12
+    cov = max(8.0 * M * N * B / hbm, 4.0 * M * M * N * B / f64)
+    jac = 24.0 * M * M * (M - 1) * EIG_SWEEPS_M16 * B / f64
+    per = (2.0 * (M - 1) + 1.0) if mirrored else 4.0 * (M - 1)
+    scan = len(ALGS) * per * L * B / f64
+    return 1e3 * (cov + jac + scan)
+
+
 def main():
     args = parse()
     from synth import get_config
@@ -207,8 +363,19 @@ def main():
         return run_reference(args, cfg)
 
     ws, rank, local = dist_env()
-    B = args.frames or cfg.B
-    frames = range(rank * B, (rank + 1) * B)      # == dist.weak_range(B, rank): own batch per rank
+    from paper_2007_14135_b200 import dist as pdist_
+    # Strong scaling (default for batched workloads): BASELINE configs[3] fixes the batch (65536
+    # frames) and shards it across the GPUs; weak: every rank owns its own full batch; single-frame
+    # configs run as independent replicas (nothing to shard).
+    total = args.frames or cfg.B
+    scaling = args.scaling if args.scaling != "auto" else ("strong" if total > 1 else "weak")
+    if scaling == "strong":
+        frames = pdist_.shard_range(total, ws, rank)
+        total_frames = total
+    else:
+        frames = pdist_.weak_range(total, rank)
+        total_frames = total * ws
+    B = len(frames)
     # generate this rank's frames BEFORE touching CUDA (the generator forks worker processes)
     from synth import generate
     t0 = time.perf_counter()
@@ -217,131 +384,55 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # DOA_BENCH_ONE_GPU / DOA_BENCH_BACKEND=gloo: test hooks that run the multi-rank path as several
+    # processes on one GPU (NCCL refuses two ranks on one device); the driver's runs use neither
+    if os.environ.get("DOA_BENCH_ONE_GPU"):
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("DOA_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")    # communicator log (NVLS / NVLink paths) on stderr
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     import paper_2007_14135_b200 as doa
     from paper_2007_14135_b200 import binding as bd
-    from paper_2007_14135_b200 import dist as pdist
 
     Xh = torch.from_numpy(Xh_np).pin_memory()
     del Xh_np
     X = Xh.to(dev)
-    M, D, L = cfg.M, cfg.D, cfg.L
-    if is_array:
-        plans = [doa.Plan.array(cfg.pos, D, a, cfg.az0, cfg.daz, cfg.naz, cfg.el0, cfg.del_, cfg.nel, cfg.az_wrap,
-                                max_batch=B, device=dev) for a in ALGS]
+    D, L = cfg.D, cfg.L
+    wl = Workload(cfg, is_array, X, B, dev, doa)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+
+    if ws > 1:
+        gbuf = torch.empty((ws, len(ALGS), max(pdist_.shard_sizes(total_frames if scaling == "strong" else B * ws, ws)),
+                            2 * D + 2), dtype=torch.int32, device=dev)
+        gout = torch.empty((len(ALGS), total_frames, 2 * D + 2), dtype=torch.int32, device=dev)
+
+        def gather(w):
+            if scaling == "strong":
+                pdist_.gather_sharded(w.packed, total_frames, out=gout, buf=gbuf)
+            else:
+                pdist_.gather_peaks(w.packed, out=gbuf)
     else:
-        plans = [doa.Plan(M, D, a, cfg.dtheta, L=L, theta0=cfg.theta0, d_over_lambda=cfg.d_over_lambda,
-                          max_batch=B, device=dev) for a in ALGS]
-    R = torch.empty((B, M, M), dtype=torch.complex128, device=dev)
-    lam = torch.empty((B, M), dtype=torch.float64, device=dev)
-    V = torch.empty((B, M, M), dtype=torch.complex128, device=dev)
-    info_eig = torch.empty((B,), dtype=torch.int32, device=dev)
-    info = torch.empty((len(ALGS), B), dtype=torch.int32, device=dev)
-    idx = torch.empty((len(ALGS), B, D), dtype=torch.int32, device=dev)
-    val = torch.empty((len(ALGS), B, D), dtype=torch.float32, device=dev)
-    npk = torch.empty((len(ALGS), B), dtype=torch.int32, device=dev)
-    gathered = None
-    if ws > 1:
-        gathered = torch.empty((ws, len(ALGS), B, 2 * D + 2), dtype=torch.int32, device=dev)
-        packed = torch.empty((len(ALGS), B, 2 * D + 2), dtype=torch.int32, device=dev)
-    stream = torch.cuda.current_stream(dev)
-    s = stream.cuda_stream
-    spec_ev = []   # (start, end) events around each doa_spectrum call (coefficients + scan kernel)
+        def gather(w):
+            return None
 
-    def step(sh, record=False):
-        """One step on stream handle `sh`; returns the number of libdoa kernel launches."""
-        launches = 0
-        bd.doa_covariance(plans[0].h, X, R, sh)
-        launches += bd.doa_last_launch_count()
-        bd.doa_eig(plans[0].h, R, lam, V, info_eig, sh)
-        launches += bd.doa_last_launch_count()
-        for a, p in enumerate(plans):
-            info[a].copy_(info_eig)
-            if record:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-            bd.doa_spectrum(p.h, lam, V, info[a], None, sh)
-            launches += bd.doa_last_launch_count()
-            if record:
-                e1.record(stream)
-                spec_ev.append((e0, e1))
-            bd.doa_peaks(p.h, B, idx[a], val[a], npk[a], info[a], sh)
-            launches += bd.doa_last_launch_count()
-        if ws > 1:
-            pdist.pack_peaks(idx, val, npk, info, out=packed)
-            pdist.gather_peaks(packed, out=gathered)
-        return launches
-
-    # CUDA graph: the step is a fixed sequence of async ABI calls on one stream, so it can be
-    # captured once and replayed (removes the ~10 us per-launch CPU overhead that dominates
-    # single-frame workloads).  Default: on for single-GPU runs.
-    use_graph = args.graph == "on" or (args.graph == "auto" and ws == 1)
-    for _ in range(max(3, args.warmup)):
-        step(s)
-    torch.cuda.synchronize()
-    graph = None
-    launches_per_step = 0
-    if use_graph:
-        for _ in range(min(args.steps, 5)):           # per-launch timing of doa_spectrum, outside the graph
-            step(s, record=True)
-        torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            launches_per_step = step(torch.cuda.current_stream().cuda_stream)
-        for _ in range(max(3, args.warmup)):
-            graph.replay()
-        torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    launches = 0
-    for _ in range(args.steps):
-        if graph is not None:
-            graph.replay()
-            launches += launches_per_step
-        else:
-            launches += step(s, record=True)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    clk = clocks.stop()
-    if ws > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        dist.barrier()
-    ms_step = ms / args.steps
-    total_frames = B * ws
+    use_graph = args.graph in ("on", "auto")
+    ms_step, launches, graph, clk = timed_steps(args, wl, ws, dev, stream, use_graph, gather)
     value = total_frames / (ms_step / 1e3)
 
-    # roofline of the dominant kernel: the scan (S4-S6) inside doa_spectrum.  On a symmetric grid
-    # (DESIGN.md Q26) the scan evaluates each mirrored angle pair with one contraction, so the
-    # algorithmic work per angle is half that of the per-angle form.
     mirrored = (not is_array and cfg.theta0 + float(L - 1) * cfg.dtheta == -cfg.theta0
                 and os.environ.get("DOA_SCAN_MIRROR", "1") != "0")
-    spec_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in spec_ev)
-    if is_array:                                   # K - 1 = M(M-1) fp64 FMAs per (frame, grid point)
-        scan_flops = 2.0 * M * (M - 1) * L * B
-    elif mirrored:                                 # per mirrored pair: E and O (2(M-1) FMAs), E +- O (2 adds)
-        scan_flops = (2.0 * (M - 1) + 1.0) * L * B
-    else:                                          # 2(M-1) fp64 FMAs per (frame, angle)
-        scan_flops = 4.0 * (M - 1) * L * B
-    pk = peaks_json()
-    fp64_peak = 148 * 64 * 2 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12   # TFLOP/s, guide unit counts
-    achieved = scan_flops / (spec_ms / 1e3) / 1e12
+    spec_ms, scan_flops, achieved, fp64_peak = scan_roofline(wl, is_array, mirrored)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath) and cfg.name == "c4":
+    if os.path.exists(tpath) and cfg.name == "c4" and B == cfg.B:
         with open(tpath) as fh:
             traffic = json.load(fh).get("scan", {}).get("traffic_bytes")
     roofline = {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
@@ -354,16 +445,38 @@ def main():
                 "kernel_ms": spec_ms, "share_of_step": spec_ms * len(ALGS) / ms_step,
                 "peak_source": "148 SMs x 64 FP64 lanes x 2 flop x sm_max_mhz (guide unit counts; "
                                "measured DMMA 37.18 / DFMA 34.19 TFLOP/s in profiles/fp64_peaks_r01.txt)"}
+    if not is_array:
+        roofline["step_roofline_ms"] = step_roofline_ms(cfg, B, mirrored, fp64_peak)
+        roofline["step_frac"] = roofline["step_roofline_ms"] / ms_step
+
+    # north-star workload (c4's frames on the 0.001-degree grid) measured in the same run
+    north = None
+    if args.north_star and cfg.name == "c4" and not is_array:
+        ncfg = get_config("ns")
+        if ws == 1 or scaling == "strong":
+            nwl = Workload(ncfg, False, X, B, dev, doa)
+            nargs = argparse.Namespace(**vars(args))
+            nargs.steps = max(2, min(args.steps, 5))
+            n_ms, _, ngraph, nclk = timed_steps(nargs, nwl, ws, dev, stream, use_graph, gather)
+            n_spec, _, n_ach, _ = scan_roofline(nwl, False, mirrored)
+            n_roof = step_roofline_ms(ncfg, B, mirrored, fp64_peak)
+            north = {"workload": "ns", "L": ncfg.L, "dtheta_deg": ncfg.dtheta, "frames": total_frames,
+                     "value": total_frames / (n_ms / 1e3), "unit": "frames/s", "ms_per_step": n_ms,
+                     "steps": nargs.steps, "points_per_s": total_frames / (n_ms / 1e3) * ncfg.L * len(ALGS),
+                     "step_roofline_ms": n_roof, "step_frac": n_roof / n_ms,
+                     "doa_spectrum_ms": n_spec, "doa_spectrum_frac": n_ach / fp64_peak, "clocks": nclk}
+            del ngraph, nwl
 
     # end to end: host (pinned) -> device copies + the step + peak lists back, via doa_run_host
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and B > 0:
         n_alg = len(ALGS)
         hidx = torch.empty((n_alg, B, D), dtype=torch.int32)
         hval = torch.empty((n_alg, B, D), dtype=torch.float32)
         hnpk = torch.empty((n_alg, B), dtype=torch.int32)
         hinfo = torch.empty((n_alg, B), dtype=torch.int32)
-        hs = [p.h for p in plans]
+        hs = [p.h for p in wl.plans]
+        s = stream.cuda_stream
         for _ in range(2):
             bd.doa_run_host(hs, Xh, hidx, hval, hnpk, hinfo, s)
         if ws > 1:
@@ -379,29 +492,33 @@ def main():
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
         if ws > 1:
-            t = torch.tensor([ems], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+            ems = max_over_ranks(ems, dev)
         ems /= k2
         # consistency: the host path returns the device path's peak lists
-        same = bool(torch.equal(hidx, idx.cpu()))
+        same = bool(torch.equal(hidx, wl.idx.cpu()))
         e2e = {"value": total_frames / (ems / 1e3), "unit": "frames/s", "ms_per_step": ems,
-               "h2d_bytes_per_step": int(Xh.numel() * 8),
-               "d2h_bytes_per_step": int(hidx.numel() * 4 + hval.numel() * 4 + hnpk.numel() * 4 + hinfo.numel() * 4),
-               "api": "doa_run_host (4 plans)", "matches_device_path": same}
+               "h2d_bytes_per_step": int(Xh.numel() * 8) * (ws if scaling == "strong" else 1),
+               "d2h_bytes_per_step": int(hidx.numel() * 4 + hval.numel() * 4 + hnpk.numel() * 4 + hinfo.numel() * 4)
+               * (ws if scaling == "strong" else 1),
+               "api": "doa_run_host (4 plans)", "matches_device_path": same,
+               "bytes_note": "whole job (all ranks' shards)" if scaling == "strong" else "per rank"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not is_array:
         cpu = oracle_baseline(cfg, args.cpu_seconds)
 
     if rank == 0:
+        cfgd = config_dict(cfg, B, ws)
+        cfgd["global_batch"] = total_frames
+        cfgd["scaling_split"] = (f"{total_frames} frames split into {ws} contiguous shards (dist.shard_range)"
+                                 if scaling == "strong" else f"{B} frames per rank")
         line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": config_dict(cfg, B, ws),
+                "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": cfgd,
                 "points_per_s": value * L * len(ALGS),
-                "roofline": roofline, "cpu_baseline": cpu, "clocks": clk, "e2e": e2e,
-                "gpu_launches": launches, "cuda_graph": bool(use_graph), "gen_seconds": gen_s}
+                "roofline": roofline, "north_star": north, "cpu_baseline": cpu, "clocks": clk, "e2e": e2e,
+                "gpu_launches": launches, "cuda_graph": graph is not None, "gen_seconds": gen_s}
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()

@@ -26,6 +26,8 @@
  *  - B == 0 is valid and enqueues nothing.
  *  - Per-frame numerical conditions never fail a call; they set bits of the caller's
  *    info[b] (DOA_INFO_*): doa_eig overwrites info[b]; doa_spectrum and doa_peaks OR into it.
+ *  - A plan belongs to the CUDA device that was current when it was created; every call on it
+ *    must be made with that device current, else DOA_ERR_INVALID_ARG (nothing enqueued).
  *  - A plan owns only its workspace (candidate lists and, for doa_run, R / lambda / V /
  *    coefficient scratch for max_batch frames).  One plan must not be used from two streams
  *    at once; doa_peaks consumes the candidates written by the preceding doa_spectrum on the
@@ -101,6 +103,16 @@ doa_status_t doa_plan_destroy(doa_plan_t plan);
 
 /* Number of candidate slots per frame the plan reserves (>= 2*((M-1)*ceil(2 d/lambda)+1)). */
 int32_t doa_plan_capacity(doa_plan_t plan);
+
+/* The plan's parameters, for callers that validate their buffers against it (the Python binding
+ * does): M, D, alg, geom (0 = ULA, 1 = general array), the CUDA device ordinal the plan (and its
+ * workspace) belongs to, candidate capacity, L (grid points) and max_batch.  Host-only, no
+ * synchronisation.  NULL plan or out -> DOA_ERR_INVALID_ARG. */
+typedef struct {
+  int32_t M, D, alg, geom, device, capacity;
+  int64_t L, max_batch;
+} doa_plan_info_t;
+doa_status_t doa_plan_info(doa_plan_t plan, doa_plan_info_t* out);
 
 /* S1 — sample covariance, Eq. 3 / Table 2 Step-1:
  *   R[b] = (1/N) sum_n x_b[n] x_b[n]^H   (1/N, Q20).

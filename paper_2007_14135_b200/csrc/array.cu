@@ -236,14 +236,10 @@ template <int M>
 cudaError_t launch_scan_array_t(const doa_plan_s* p, int64_t B, cudaStream_t s) {
   using Sh = ArrShape<M>;
   const size_t smem = (size_t)Sh::NB * Sh::S * Sh::NA * 32 * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(scan_array_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  kernel_occupancy(scan_array_kernel<M>, kArrWarps * 32, smem);     // sets the smem attribute on this device
   const int64_t cols = (p->L + Sh::NB * Sh::W - 1) / (Sh::NB * Sh::W);
   const int64_t ngroups = (B + 7) / 8;
-  int64_t per = (cols * ngroups) / (148 * 8);
+  int64_t per = (cols * ngroups) / ((int64_t)sm_count() * 8);
   if (per < 8) per = 8;
   if (per > ngroups) per = ngroups;
   const int64_t gy = (ngroups + per - 1) / per;

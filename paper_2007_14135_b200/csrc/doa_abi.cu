@@ -33,9 +33,12 @@ doa_status_t cuda_fail(cudaError_t e, const char* where) {
 
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
-#define DOA_CHECK_PLAN(p)                                                   \
-  do {                                                                      \
-    if (!(p)) return fail(DOA_ERR_INVALID_ARG, "%s: plan is NULL", __func__); \
+#define DOA_CHECK_PLAN(p)                                                                          \
+  do {                                                                                             \
+    if (!(p)) return fail(DOA_ERR_INVALID_ARG, "%s: plan is NULL", __func__);                      \
+    if (doa::current_device() != (p)->device)                                                      \
+      return fail(DOA_ERR_INVALID_ARG, "%s: plan was created on device %d, current device is %d", \
+                  __func__, (p)->device, doa::current_device());                                   \
   } while (0)
 #define DOA_CHECK_PTR(ptr, al)                                                                         \
   do {                                                                                                 \
@@ -142,6 +145,7 @@ doa_status_t doa_plan_create(doa_plan_t* plan, int32_t M, double d_over_lambda, 
 
   doa_plan_s* p = new doa_plan_s();
   std::memset(p, 0, sizeof *p);
+  p->device = doa::current_device();
   p->M = M; p->D = D; p->alg = alg; p->dl = d_over_lambda; p->theta0 = theta0_deg; p->dtheta = dtheta_deg;
   p->L = L; p->max_batch = max_batch;
   // Q26: a grid whose last point (Q8 arithmetic) is exactly -theta0 is built from both ends and the
@@ -196,6 +200,7 @@ doa_status_t doa_plan_create_array(doa_plan_t* plan, int32_t M, const double* po
 
   doa_plan_s* p = new doa_plan_s();
   std::memset(p, 0, sizeof *p);
+  p->device = doa::current_device();
   p->M = M; p->D = D; p->alg = alg; p->geom = 1;
   p->az0 = az0_deg; p->daz = daz_deg; p->naz = naz; p->el0 = el0_deg; p->del = del_deg; p->nel = nel;
   p->wrap = az_wrap ? 1 : 0;
@@ -227,6 +232,9 @@ doa_status_t doa_plan_create_array(doa_plan_t* plan, int32_t M, const double* po
 
 doa_status_t doa_plan_destroy(doa_plan_t p) {
   if (!p) return DOA_OK;
+  const int cur = doa::current_device();
+  const int dev = p->device;
+  if (cur != dev) cudaSetDevice(dev);                   // free on the plan's device
   cudaDeviceSynchronize();
   cudaFree(p->dpos); cudaFree(p->fbuf);
   cudaFree(p->cnt); cudaFree(p->cand_idx); cudaFree(p->cand_f); cudaFree(p->coef);
@@ -238,10 +246,19 @@ doa_status_t doa_plan_destroy(doa_plan_t p) {
     if (p->ev_used[k]) cudaEventDestroy(p->ev_used[k]);
   }
   delete p;
+  if (cur != dev) cudaSetDevice(cur);
   return DOA_OK;
 }
 
 int32_t doa_plan_capacity(doa_plan_t p) { return p ? p->cap : 0; }
+
+doa_status_t doa_plan_info(doa_plan_t p, doa_plan_info_t* out) {
+  if (!p) return fail(DOA_ERR_INVALID_ARG, "doa_plan_info: plan is NULL");
+  if (!out) return fail(DOA_ERR_INVALID_ARG, "doa_plan_info: out is NULL");
+  out->M = p->M; out->D = p->D; out->alg = p->alg; out->geom = p->geom; out->device = p->device;
+  out->capacity = p->cap; out->L = p->L; out->max_batch = p->max_batch;
+  return DOA_OK;
+}
 
 doa_status_t doa_covariance(doa_plan_t p, const float* X, int64_t B, int64_t N, double* R, doa_stream_t s) {
   g_launches = 0;
@@ -330,6 +347,9 @@ doa_status_t doa_run_host(const doa_plan_t* plans, int32_t nplans, const float* 
   if (!plans || nplans < 1) return fail(DOA_ERR_INVALID_ARG, "doa_run_host: need nplans >= 1 plans");
   for (int k = 0; k < nplans; ++k) {
     if (!plans[k]) return fail(DOA_ERR_INVALID_ARG, "doa_run_host: plans[%d] is NULL", k);
+    if (plans[k]->device != doa::current_device())
+      return fail(DOA_ERR_INVALID_ARG, "doa_run_host: plans[%d] was created on device %d, current device is %d", k,
+                  plans[k]->device, doa::current_device());
     if (plans[k]->M != plans[0]->M || plans[k]->D != plans[0]->D)
       return fail(DOA_ERR_INVALID_ARG, "doa_run_host: plans must share M and D");
     DOA_CHECK_B(plans[k], B);

@@ -39,6 +39,7 @@ inline size_t coef_words(int64_t max_batch, int M) { return (size_t)((max_batch 
 
 struct doa_plan_s {
   int32_t M, D, alg, cap;
+  int32_t device;                 // CUDA device the plan's workspace lives on; calls must run there
   int32_t geom;                   // 0: ULA (Toeplitz scan); 1: general array on an az x el grid
   double dl, theta0, dtheta;
   int64_t L, max_batch;
@@ -91,5 +92,16 @@ cudaError_t launch_generate(int M, double dl, int D, const double* theta, int pe
                             int64_t frame0, int64_t B, int64_t N, float* X, cudaStream_t s);
 
 void count_launch();
+
+// Per-device launch configuration (csrc/runtime.cu): SM count of the current device, and the
+// occupancy of `func` at (threads, smem) on the current device — setting its dynamic-smem
+// attribute there first when smem > 48 KB.  Cached per (kernel, device); thread-safe.
+int current_device();
+int sm_count();
+int kernel_occupancy(const void* func, int threads, size_t smem);
+template <typename F>
+inline int kernel_occupancy(F* func, int threads, size_t smem) {
+  return kernel_occupancy(reinterpret_cast<const void*>(func), threads, smem);
+}
 
 }  // namespace doa

@@ -40,17 +40,8 @@ namespace {
 constexpr int kN = 16;            // padded order
 constexpr int kLd = 17;           // smem row stride (double2)
 constexpr int kEigWarps = 4;
-#ifndef DOA_EIG_PARAM
-#define DOA_EIG_PARAM 1       // short-chain rotation parameters (see phase 1)
-#endif
 #ifndef DOA_EIG_HALF_MIN_B
 #define DOA_EIG_HALF_MIN_B 2048  // below this batch size M > 8 uses eig16_kernel
-#endif
-#ifndef DOA_EIG_N8
-#define DOA_EIG_N8 1          // M <= 8: 8-index round robin (eig16h_kernel<8>)
-#endif
-#ifndef DOA_EIG_HALF
-#define DOA_EIG_HALF 1        // two matrices per warp, one per half (eig16h_kernel)
 #endif
 #ifndef DOA_EIG_MINB
 #define DOA_EIG_MINB 5
@@ -62,17 +53,12 @@ __device__ __forceinline__ int aidx(int i, int j) { return i * kLd + (j ^ (i >> 
 __device__ constexpr int kBlockOrder[28] = {14, 11, 10, 16, 13, 8, 25, 15, 4, 6, 19, 12, 21, 26,
                                              1, 17, 18, 7, 23, 24, 22, 20, 9, 27, 3, 2, 0, 5};
 
-// Rotation parameters of one slot pair.  Padded to 48 bytes (DOA_EIG_PRMPAD) so the eight pairs'
+// Rotation parameters of one slot pair.  Padded to 48 bytes so the eight pairs'
 // 16-byte halves fall in distinct shared-memory banks: phase 2b's loads (pairs k and k+4 in one
 // instruction) and phase 2a's (pairs rb, sb over 28 lanes) are single wavefronts.
-#ifndef DOA_EIG_PRMPAD
-#define DOA_EIG_PRMPAD 1
-#endif
 struct __align__(16) Prm {
   double c, s, er, ei;
-#if DOA_EIG_PRMPAD
   double pad0, pad1;
-#endif
 };
 
 __device__ __forceinline__ double wsum(double v) {
@@ -203,11 +189,7 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
       if (off <= tol) break;
       if (sweep == kMaxSweeps) { flag |= DOA_INFO_NOCONV; break; }
     }
-#if DOA_EIG_UNROLL
-#pragma unroll
-#else
 #pragma unroll 1
-#endif
     for (int rnd = 0; rnd < kN - 1; ++rnd) {
       const double2* A = As[warp][cur];
       double2* An = As[warp][cur ^ 1];
@@ -226,7 +208,6 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
         }
         const double r2 = axy.x * axy.x + axy.y * axy.y;
         const bool rot = r2 > 1e-300;                         // a_xy ~ 0: identity rotation
-#if DOA_EIG_PARAM
         // Short-chain parameters (same rotation as GvL sym.schur2): with d = (a_yy - a_xx)/2,
         // r = |a_xy|, h = sqrt(d^2 + r^2), q = |d| + h:  t = sign(d) r / q,  c = sqrt(q / 2h),
         // s = sign(d) r / sqrt(2 h q)  (c^2 + s^2 = 1 exactly in exact arithmetic), t r = sign(d) r^2 / q.
@@ -248,51 +229,11 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
         p.s = rot ? (d < 0.0 ? -sabs : sabs) : 0.0;
         p.er = rot ? axy.x * ir : 1.0;
         p.ei = rot ? -axy.y * ir : 0.0;
-#else
-        const double ir = rsqrt_pos(rot ? r2 : 1.0);          // 1/|a_xy|
-        const double rr = r2 * ir;                            // |a_xy|
-        const double tau = (ayy - axx) * (0.5 * ir);
-#if DOA_EIG_F32_ANGLE
-        // The rotation ANGLE only needs to be close to the zeroing one: t is computed in fp32
-        // (short MUFU latency), then c = 1/sqrt(1 + t^2), s = t c in fp64 keep J exactly unitary,
-        // and the 2x2 diagonal block is rotated explicitly (its tiny off-diagonal remainder stays
-        // in A and is removed by later sweeps; same stop rule).
-        const float atf = fabsf((float)tau);
-        float tf = __frcp_rn(atf > 1e18f ? 2.0f * atf : atf + __fsqrt_rn(fmaf(atf, atf, 1.0f)));
-        double t = rot ? (tau < 0.0 ? -(double)tf : (double)tf) : 0.0;
-#else
-        const double at = fabs(tau);
-        const double atc = fmin(at, 1e150);
-        const double w = fma(atc, atc, 1.0);
-        // 1/(|tau| + sqrt(1 + tau^2)); -> 1/(2|tau|) once tau^2 would overflow
-        double t = rcp_pos(fmin(at > 1e150 ? 2.0 * at : atc + w * rsqrt_pos(w), 1e300));
-        t = rot ? (tau < 0.0 ? -t : t) : 0.0;
-#endif
-        Prm p;
-        p.c = rot ? rsqrt_pos(fma(t, t, 1.0)) : 1.0;
-        p.s = t * p.c;
-        p.er = rot ? axy.x * ir : 1.0;
-        p.ei = rot ? -axy.y * ir : 0.0;
-#endif
         if (lane < 8) {
           prm[warp][lane] = p;
-#if DOA_EIG_F32_ANGLE
-          const double cc = p.c * p.c, ss = p.s * p.s, cs = p.c * p.s;
-          An[wxx] = make_double2(cc * axx - 2.0 * cs * rr + ss * ayy, 0.0);
-          An[wyy] = make_double2(ss * axx + 2.0 * cs * rr + cc * ayy, 0.0);
-          // (G^T B G)_12 = cs (a_xx - a_yy) + (c^2 - s^2) |a_xy|, real in the rotated basis; stored at
-          // (min, max) of the permuted pair, conjugation of a real value is a no-op
-          An[wxy] = make_double2(cs * (axx - ayy) + (cc - ss) * rr, 0.0);
-#else
-#if DOA_EIG_PARAM
           An[wxx] = make_double2(axx - tr, 0.0);
           An[wyy] = make_double2(ayy + tr, 0.0);
-#else
-          An[wxx] = make_double2(axx - t * rr, 0.0);
-          An[wyy] = make_double2(ayy + t * rr, 0.0);
-#endif
           An[wxy] = make_double2(0.0, 0.0);
-#endif
         }
       }
       __syncwarp();
@@ -370,7 +311,7 @@ __global__ void __launch_bounds__(kEigWarps * 32, DOA_EIG_MINB) eig16_kernel(con
   if (lane == 0) info[b] = flag;
 }
 
-// Half-warp variant (DOA_EIG_HALF): two matrices per warp, one per 16-lane half.  Phase 1 of both
+// Half-warp variant: two matrices per warp, one per 16-lane half.  Phase 1 of both
 // matrices runs in the same instructions (lanes 0-7 and 16-23), so the redundant rotation lanes
 // drop from 24 to 16 per matrix; each lane of a half owns one full row of V (16 complex) and two
 // of the 28 off-diagonal blocks.  A converged matrix keeps running with identity rotations
@@ -419,7 +360,10 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
   const bool valid = b < B;
   Prm* pm = prm[warp][hm];
 
-  double nrm = 0.0;
+  // ||R||_F and off(A) are summed in the same order as eig16_kernel's (lane partials over the
+  // element strides of 32, i.e. this half-lane's even and odd strides of 16, added, then the tree),
+  // so both kernels take identical stop decisions and a frame's results do not depend on B.
+  double nrm_e = 0.0, nrm_o = 0.0;
   {
     const double2* Rb = R + (size_t)(valid ? b : 0) * M * M;
     for (int e = hl; e < N * N; e += 16) {
@@ -429,10 +373,11 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
       if (valid && j < M) v = Rb[(size_t)i * M + j];
       if (i == j) v.y = 0.0;
       As[warp][hm][0][aidxT<N>(i, j)] = v;
-      nrm += (i == j ? 1.0 : 2.0) * (v.x * v.x + v.y * v.y);
+      const double t = (i == j ? 1.0 : 2.0) * (v.x * v.x + v.y * v.y);
+      if ((e / 16) & 1) nrm_o += t; else nrm_e += t;
     }
   }
-  const double tol = 10.0 * DBL_EPSILON * sqrt(hsum(nrm));
+  const double tol = 10.0 * DBL_EPSILON * sqrt(hsum(nrm_e + nrm_o));
 
   double2 v[N];                                           // row hl of this half's V
 #pragma unroll
@@ -478,12 +423,15 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
   for (int sweep = 0;; ++sweep) {
     {
       const double2* A = As[warp][hm][cur];
-      double off = 0.0;
+      double off_e = 0.0, off_o = 0.0;
       for (int e = hl; e < N * N; e += 16) {
         const int i = e / N, j = e % N;
-        if (i < j) { const double2 a = A[aidxT<N>(i, j)]; off += a.x * a.x + a.y * a.y; }
+        if (i < j) {
+          const double2 a = A[aidxT<N>(i, j)];
+          if ((e / 16) & 1) off_o += a.x * a.x + a.y * a.y; else off_e += a.x * a.x + a.y * a.y;
+        }
       }
-      off = sqrt(2.0 * hsum(off));
+      const double off = sqrt(2.0 * hsum(off_e + off_o));
       if (act && off <= tol) act = false;
       else if (act && sweep == kMaxSweeps) { flag |= DOA_INFO_NOCONV; act = false; }
     }
@@ -589,9 +537,9 @@ cudaError_t launch_eig16(const double* R, int64_t B, int M, double* lam, double*
   // small batches of M > 8 (latency-bound single frames) take the one-warp-per-matrix kernel,
   // whose single-matrix round is shorter; it performs the same operations in the same order, so
   // the results are bitwise the same (tests/test_gpu_parity.py::test_eig_kernels_bitwise_equal)
-  if (DOA_EIG_HALF && (M <= 8 || B >= DOA_EIG_HALF_MIN_B)) {
+  if (M <= 8 || B >= DOA_EIG_HALF_MIN_B) {
     const unsigned g = (unsigned)((B + 2 * kHWarps - 1) / (2 * kHWarps));
-    if (M <= 8 && DOA_EIG_N8)
+    if (M <= 8)
       eig16h_kernel<8><<<g, kHWarps * 32, 0, s>>>(reinterpret_cast<const double2*>(R), B, M, lam,
                                                    reinterpret_cast<double2*>(V), info);
     else

@@ -20,9 +20,6 @@
 namespace doa {
 namespace {
 
-#ifndef DOA_EIG_PARAM
-#define DOA_EIG_PARAM 1       // short-chain rotation parameters (as eig16)
-#endif
 
 struct PrmN {
   double c, s, er, ei;
@@ -192,7 +189,6 @@ __global__ void __launch_bounds__(EigN<N>::T, 1) eigN_kernel(const double2* __re
         const double axx = A[rxx].x, ayy = A[ryy].x;
         const double r2 = axy.x * axy.x + axy.y * axy.y;
         const bool rot = r2 > 1e-300;                         // a_xy ~ 0: identity rotation
-#if DOA_EIG_PARAM
         // Short-chain parameters (same rotation as GvL sym.schur2): with d = (a_yy - a_xx)/2,
         // r = |a_xy|, h = sqrt(d^2 + r^2), q = |d| + h:  t = sign(d) r / q,  c = sqrt(q / 2h),
         // s = sign(d) r / sqrt(2 h q)  (c^2 + s^2 = 1 exactly in exact arithmetic), t r = sign(d) r^2 / q.
@@ -214,30 +210,10 @@ __global__ void __launch_bounds__(EigN<N>::T, 1) eigN_kernel(const double2* __re
         p.s = rot ? (d < 0.0 ? -sabs : sabs) : 0.0;
         p.er = rot ? axy.x * ir : 1.0;
         p.ei = rot ? -axy.y * ir : 0.0;
-#else
-        const double ir = rsqrt_p(rot ? r2 : 1.0);
-        const double rr = r2 * ir;
-        const double tau = (ayy - axx) * (0.5 * ir);
-        const double at = fabs(tau);
-        const double atc = fmin(at, 1e150);
-        const double w = fma(atc, atc, 1.0);
-        double t = rcp_p(fmin(at > 1e150 ? 2.0 * at : atc + w * rsqrt_p(w), 1e300));
-        t = rot ? (tau < 0.0 ? -t : t) : 0.0;
-        PrmN p;
-        p.c = rot ? rsqrt_p(fma(t, t, 1.0)) : 1.0;
-        p.s = t * p.c;
-        p.er = rot ? axy.x * ir : 1.0;
-        p.ei = rot ? -axy.y * ir : 0.0;
-#endif
         prm_cs[prm_slot<N>(tid)] = make_double2(p.c, p.s);
         prm_ee[prm_slot<N>(tid)] = make_double2(p.er, p.ei);
-#if DOA_EIG_PARAM
         An[wxx] = make_double2(axx - tr, 0.0);
         An[wyy] = make_double2(ayy + tr, 0.0);
-#else
-        An[wxx] = make_double2(axx - t * rr, 0.0);
-        An[wyy] = make_double2(ayy + t * rr, 0.0);
-#endif
         An[wxy] = make_double2(0.0, 0.0);
       }
       __syncthreads();
@@ -315,11 +291,7 @@ __global__ void __launch_bounds__(EigN<N>::T, 1) eigN_kernel(const double2* __re
 template <int N>
 cudaError_t launch_eigN_t(const double* R, int64_t B, int M, double* lam, double* V, int32_t* info, cudaStream_t s) {
   const size_t smem = (size_t)2 * N * EigN<N>::LD * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(eigN_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  kernel_occupancy(eigN_kernel<N>, EigN<N>::T, smem);               // sets the smem attribute on this device
   count_launch();
   eigN_kernel<N><<<(unsigned)B, EigN<N>::T, smem, s>>>(reinterpret_cast<const double2*>(R), B, M, lam,
                                                        reinterpret_cast<double2*>(V), info);

@@ -105,12 +105,8 @@ cudaError_t launch_generate(int M, double dl, int D, const double* theta, int pe
   const double sigma = std::sqrt(std::pow(10.0, -snr_db / 10.0));
   const dim3 grid((unsigned)B, (unsigned)((N + kGenThreads - 1) / kGenThreads));
   const size_t smem = (size_t)M * D * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(generate_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * kMaxGenD * 16);
-    attr = true;
-  }
   auto go = [&](auto kern) {
+    kernel_occupancy(kern, kGenThreads, smem);          // sets the smem attribute on this device
     kern<<<grid, kGenThreads, smem, s>>>(M, dl, D, theta, per_frame, sigma, (uint32_t)seed, (uint32_t)(seed >> 32),
                                         frame0, N, reinterpret_cast<float2*>(X));
   };

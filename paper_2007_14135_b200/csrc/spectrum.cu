@@ -22,120 +22,6 @@ __device__ __forceinline__ float to_p32(double f) {
   return p > (double)FLT_MAX ? FLT_MAX : (float)p;      // Q12: fp32 P saturates at FLT_MAX
 }
 
-// ---------------------------------------------------------------------------------------------
-// S3: one warp per frame.  Table 3 Step-3 noise-subspace objects as weighted vectors
-// {(w_j, u_j)}, C = sum_j w_j u_j u_j^H, and c_k = sum_j w_j sum_p u_j[p] conj(u_j[p+k]).
-//   PHD: u = e_0 (smallest eigenvalue), w = 1.     MUSIC: u_j = e_j, j < K = M-D, w = 1.
-//   EV : u_j = e_j, w_j = 1/lambda_j (Q1), clamped at 100 eps lambda_max (DEGENERATE).
-//   MN : u = P_n e1 / (e1^H P_n e1), P_n e1 = sum_j e_j conj(e_j[0]) (Q5); p0 <= 100 eps: DEGENERATE.
-// Writes the coefficients in the scan's A-fragment layout (coef_index) and zeroes the frame's
-// candidate counter for the scan that follows.
-// The frame's noise vectors are staged transposed in shared memory (U[j][p], coalesced global
-// reads of V's rows), so the lanes computing different lags k read consecutive addresses.  Lanes
-// are split into M lags x H = 32/M vector-slices (M <= 16: every lane busy); the H partial sums
-// of a lag are combined in a fixed order (deterministic).
-constexpr int kCoefWarps = 4;
-#ifndef DOA_COEF_WAVES
-#define DOA_COEF_WAVES 2      // coef_mma_kernel CTAs = resident slots x waves (persistent warps)
-#endif
-#ifndef DOA_COEF_MMA
-#define DOA_COEF_MMA 1        // M <= 16: coefficients as a DMMA product C = X U^H + diagonal sums
-#endif
-
-__global__ void __launch_bounds__(kCoefWarps * 32) coef_kernel(const double* __restrict__ lam,
-                                                              const double2* __restrict__ V, int64_t B, int M,
-                                                              int D, int alg, double* __restrict__ coef,
-                                                              int32_t* __restrict__ cnt, int32_t* __restrict__ info) {
-  extern __shared__ double2 csm[];                    // per warp: U[M][M+1], then part[32] (double2)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-  if (b >= B) return;
-  const int ld = M + 1;
-  double2* U = csm + (size_t)warp * (M * ld + 32);
-  double2* part = U + M * ld;
-  const int S = ksteps(M);
-  const double2* Vb = V + (size_t)b * M * M;
-  const double* lb = lam + (size_t)b * M;
-  const int K = M - D;
-  int flag = 0;
-  const int nload = (alg == DOA_ALG_PHD) ? 1 : K;      // columns needed
-  for (int e = lane; e < M * M; e += 32) {
-    const int p = e / M, j = e - (e / M) * M;
-    if (j < nload) U[j * ld + p] = Vb[e];
-  }
-  double lfloor = 0.0;
-  if (alg == DOA_ALG_EV) {
-    lfloor = 100.0 * DBL_EPSILON * fmax(lb[M - 1], 0.0);
-    for (int j = 0; j < K; ++j) if (lb[j] <= lfloor) flag |= DOA_INFO_DEGENERATE;
-  }
-  __syncwarp();
-  int nv = (alg == DOA_ALG_MUSIC || alg == DOA_ALG_EV) ? K : 1;
-  if (alg == DOA_ALG_MN) {
-    // w = P_n e1 / (e1^H P_n e1): P_n e1 = sum_j e_j conj(e_j[0]), e1^H P_n e1 = sum_j |e_j[0]|^2
-    double p0 = 0.0;
-    for (int j = 0; j < K; ++j) { const double2 v = U[j * ld]; p0 += v.x * v.x + v.y * v.y; }
-    const bool degen = !(p0 > 100.0 * DBL_EPSILON);
-    if (degen) flag |= DOA_INFO_DEGENERATE;
-    const double lp = degen ? 1.0 : 1.0 / p0;
-    double2 wv[2];
-    for (int rep = 0, i = lane; rep < 2; ++rep, i += 32) {
-      double pr = 0.0, pi = 0.0;
-      if (i < M)
-        for (int j = 0; j < K; ++j) {
-          const double2 e = U[j * ld + i], e0 = U[j * ld];
-          pr += e.x * e0.x + e.y * e0.y;                 // e_j[i] * conj(e_j[0])
-          pi += e.y * e0.x - e.x * e0.y;
-        }
-      wv[rep] = degen ? make_double2(pr, pi) : make_double2(pr * lp, pi * lp);
-    }
-    __syncwarp();
-    for (int rep = 0, i = lane; rep < 2; ++rep, i += 32)
-      if (i < M) U[i] = wv[rep];                        // vector 0 <- w
-    __syncwarp();
-  }
-  const int H = M <= 16 ? 32 / M : 1;                  // vector slices per lag
-  for (int k0 = 0; k0 < M; k0 += 32) {                 // M = 64: two passes of 32 lags
-    const int k = k0 + (M <= 16 ? lane % M : lane);
-    const int hh = M <= 16 ? lane / M : 0;
-    double cr = 0.0, ci = 0.0;
-    if (k < M && hh < H) {
-      for (int j = hh; j < nv; j += H) {
-        const double2* u = U + j * ld;
-        double sr = 0.0, si = 0.0;
-        for (int p = 0; p + k < M; ++p) {
-          const double2 x = u[p], y = u[p + k];          // u[p] conj(u[p+k])
-          sr += x.x * y.x + x.y * y.y;
-          si += x.y * y.x - x.x * y.y;
-        }
-        const double w = (alg != DOA_ALG_EV) ? 1.0
-                         : (lb[j] <= lfloor ? (lfloor > 0.0 ? 1.0 / lfloor : 1.0) : 1.0 / lb[j]);
-        cr += w * sr;
-        ci += w * si;
-      }
-    }
-    part[lane] = make_double2(cr, ci);
-    __syncwarp();
-    if (lane < (M <= 16 ? M : 32) && k0 + lane < M) {
-      const int kk = k0 + lane;
-      double sr = 0.0, si = 0.0;
-      for (int h2 = 0; h2 < H; ++h2) { const double2 v = part[h2 * (M <= 16 ? M : 32) + lane]; sr += v.x; si += v.y; }
-      if (kk == 0) coef[coef_index(b, 0, S)] = sr;
-      else {
-        coef[coef_index(b, coef_cos(kk), S)] = 2.0 * sr;
-        coef[coef_index(b, coef_sin(M, kk), S)] = 2.0 * si;
-      }
-    }
-    __syncwarp();
-  }
-  const int JE = 4 * ksteps_even(M);
-  for (int j = lane; j < 4 * S; j += 32)                                                // K padding
-    if ((j >= M && j < JE) || j >= JE + M - 1) coef[coef_index(b, j, S)] = 0.0;
-  if (lane == 0) {
-    cnt[b] = 0;
-    if (info && flag) info[b] |= flag;           // no read-modify-write round trip when clean
-  }
-}
-
 // T_j(psi) in the split layout of doa_internal.cuh: j = 0 -> 1; 1..M-1 -> cos(j psi);
 // JE..JE+M-2 -> sin((j-JE+1) psi) with JE = 4 ceil(M/4); else 0.
 // psi = pi u; cospi/sinpi of the exact multiple j*u (one rounding) — no recurrence.  Both are
@@ -175,6 +61,17 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
                : "d"(a), "d"(b));
 }
 
+// ---------------------------------------------------------------------------------------------
+// S3 (Table 3 Step-3/4): noise-subspace objects as weighted vectors {(w_j, u_j)},
+// C = sum_j w_j u_j u_j^H, reduced to the Toeplitz sums c_k = sum_p C[p][p+k]:
+//   PHD: u = e_0 (smallest eigenvalue), w = 1.     MUSIC: u_j = e_j, j < K = M-D, w = 1.
+//   EV : u_j = e_j, w_j = 1/lambda_j (Q1), clamped at 100 eps lambda_max (DEGENERATE, G1).
+//   MN : u = P_n e1 / (e1^H P_n e1), P_n e1 = sum_j e_j conj(e_j[0]) (Q5); p0 <= 100 eps: DEGENERATE.
+// The coefficients go to the scan's A-fragment layout (coef_index); the frame's candidate counter
+// is zeroed for the scan that follows.
+//
+constexpr int kCoefWaves = 2;     // coef_mma_kernel CTAs = resident slots x waves (persistent warps)
+
 // S3 for M <= 16 on the FP64 tensor pipe.  C = X U^H with U = the noise vectors (columns of V)
 // and X = (w_j u_j) (weights only for EV; MN: the single vector w of Table 3 Step-3), i.e.
 //   C_re = X_re U_re^T + X_im U_im^T,   C_im = X_im U_re^T - X_re U_im^T   (16 x 16, inner dim j),
@@ -182,7 +79,7 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
 // frame — with the operand fragments read once from shared memory (U staged as re/im planes
 // [j][p], row stride 20 doubles: conflict-free staging stores and fragment loads).  The tiles go back through shared memory and lanes k < M add the
 // diagonal c_k = sum_p C[p][p+k] in ascending p.  Fixed orders throughout: deterministic.  Replaces
-// the lag-per-lane loop (coef_kernel) whose shared-memory traffic (~1000 wavefronts per frame)
+// a lag-per-lane loop (round-1 coef_kernel) whose shared-memory traffic (~1000 wavefronts per frame)
 // bound it; this one moves ~150.
 constexpr int kCoefMmaWarps = 8;
 constexpr int kCoefMmaLd = 20;                         // plane row stride (doubles), = 4 mod 16: conflict-free fragments
@@ -390,7 +287,10 @@ __global__ void __launch_bounds__(kCoefBigWarps * 32) coef_big_kernel(const doub
   __syncthreads();
   int nv = (alg == DOA_ALG_MUSIC || alg == DOA_ALG_EV) ? K : 1;
   if (alg == DOA_ALG_MN) {
-    double p0 = lane < K ? Ure[lane * ld] * Ure[lane * ld] + Uim[lane * ld] * Uim[lane * ld] : 0.0;
+    // e1^H P_n e1 = sum_j |e_j[0]|^2 over all K noise vectors (K up to 63): lane-strided partial
+    // sums in ascending j, then a fixed xor tree (deterministic)
+    double p0 = 0.0;
+    for (int j = lane; j < K; j += 32) p0 += Ure[j * ld] * Ure[j * ld] + Uim[j * ld] * Uim[j * ld];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) p0 += __shfl_xor_sync(0xffffffffu, p0, o);   // fixed tree order
     const bool degen = !(p0 > 100.0 * DBL_EPSILON);
@@ -498,25 +398,8 @@ __global__ void __launch_bounds__(kCoefBigWarps * 32) coef_big_kernel(const doub
 // (A persistent tile loop, a software-pipelined and a warp-specialised producer/consumer variant
 // were measured and were slower on c4; see profiles/README.md.)
 constexpr int kCtaWarps = 8;
-// Tuning knobs (compile-time; tools/scan_variants.sh builds A/B libraries with -D overrides).
-#ifndef DOA_SCAN_NA
-#define DOA_SCAN_NA 8        // 8-angle tiles per block (a lane owns 2*NA consecutive angles)
-#endif
-#ifndef DOA_SCAN_MNB
-#define DOA_SCAN_MNB 1       // blocks per column in the mirrored scan
-#endif
-#ifndef DOA_SCAN_MINB
-#define DOA_SCAN_MINB 2      // __launch_bounds__ min blocks per SM
-#endif
-#ifndef DOA_SCAN_PP
-#define DOA_SCAN_PP 1        // ping-pong the DMMA pipe between the two warp groups of a CTA
-#endif
-#ifndef DOA_SCAN_EO
-#define DOA_SCAN_EO 1        // mirrored scan: interleave the E and O k-steps in the DMMA sequence
-#endif
-#ifndef DOA_SCAN_PF
-#define DOA_SCAN_PF 1        // prefetch the next group's A fragments into registers
-#endif
+constexpr int kScanNA = 8;        // 8-angle tiles per block (a lane owns 2*NA consecutive angles)
+constexpr int kScanMinBlocks = 2; // __launch_bounds__ min blocks per SM
 constexpr long long kInfBits = 0x7FF0000000000000LL;        // bits of +inf
 constexpr long long kFloorBits = 0x01A56E1FC2F8F359LL;      // bits of 1e-300 (kFloor, Q12)
 
@@ -527,10 +410,10 @@ constexpr long long kFloorBits = 0x01A56E1FC2F8F359LL;      // bits of 1e-300 (k
 // 64 KB of smem).
 template <int S, bool MIRROR>
 struct ScanShape {
-  static constexpr int NA = DOA_SCAN_NA;                     // 8-angle tiles per block
+  static constexpr int NA = kScanNA;                     // 8-angle tiles per block
   static constexpr int W = 8 * NA;                           // angles per block (incl. 2 halo)
   static constexpr bool STREAM_A = S > 8;
-  static constexpr int NB = STREAM_A ? 1 : (MIRROR ? DOA_SCAN_MNB : 2);   // blocks per column
+  static constexpr int NB = STREAM_A ? 1 : (MIRROR ? 1 : 2);   // blocks per column
   static constexpr int SE = MIRROR ? (S + 1) / 2 : S;        // k-steps of the even part E
 };
 
@@ -615,7 +498,7 @@ __device__ __forceinline__ void scan_epilogue(long long (&v)[2 * NA], int lane, 
 }
 
 template <int S, bool WRITE_P, bool MIRROR>
-__global__ void __launch_bounds__(kCtaWarps * 32, DOA_SCAN_MINB) scan_cta_kernel(const double* __restrict__ coef, int64_t B, int M,
+__global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kernel(const double* __restrict__ coef, int64_t B, int M,
                                                                    int64_t per, double dl, double theta0, double dtheta, int L,
                                                                    bool sym, int cap, int32_t* __restrict__ cnt,
                                                                    int32_t* __restrict__ cidx,
@@ -644,19 +527,19 @@ __global__ void __launch_bounds__(kCtaWarps * 32, DOA_SCAN_MINB) scan_cta_kernel
   const int64_t g0 = y * per;
   const int64_t g1 = (g0 + per < ngroups) ? g0 + per : ngroups;
   double an[SA];
-  if (!STREAM_A && DOA_SCAN_PF && g0 + warp < g1) {
+  if (!STREAM_A && g0 + warp < g1) {
     const double* cg = coef + ((size_t)(g0 + warp) * S) * 32 + lane;
 #pragma unroll
     for (int s = 0; s < SA; ++s) an[s] = __ldg(cg + s * 32);
   }
-  // Ping-pong (DOA_SCAN_PP): warps 0-3 and 4-7 take turns on the DMMA pipe — a warp group issues
+  // Ping-pong: warps 0-3 and 4-7 take turns on the DMMA pipe — a warp group issues
   // its block's DMMAs, hands the pipe to the other group (named barriers 1/2) and runs its
   // epilogue while the other group's DMMAs execute, so the pipe never idles on an epilogue phase
   // that all warps would otherwise reach together.  Trip counts are CTA-uniform (warps past the
   // chunk's last group still take their turns, without work).
   const int wg = warp >> 2;
   const int64_t nit = (g1 - g0 + kCtaWarps - 1) / kCtaWarps;
-  if (DOA_SCAN_PP && wg == 1) bar_arrive(1);
+  if (wg == 1) bar_arrive(1);
   for (int64_t it = 0; it < nit; ++it) {
     const int64_t g = g0 + warp + it * kCtaWarps;
     const bool gv = g < g1;                                      // warp-uniform
@@ -664,8 +547,8 @@ __global__ void __launch_bounds__(kCtaWarps * 32, DOA_SCAN_MINB) scan_cta_kernel
     double a[SA];
     if (!STREAM_A && gv) {
 #pragma unroll
-      for (int s = 0; s < SA; ++s) a[s] = DOA_SCAN_PF ? an[s] : __ldg(cgc + s * 32);
-      if (DOA_SCAN_PF && g + kCtaWarps < g1) {                                // prefetch the next group's operands
+      for (int s = 0; s < SA; ++s) a[s] = an[s];
+      if (g + kCtaWarps < g1) {                                // prefetch the next group's operands
         const double* cg = coef + ((size_t)(g + kCtaWarps) * S) * 32 + lane;
 #pragma unroll
         for (int s = 0; s < SA; ++s) an[s] = __ldg(cg + s * 32);
@@ -685,9 +568,9 @@ __global__ void __launch_bounds__(kCtaWarps * 32, DOA_SCAN_MINB) scan_cta_kernel
 #pragma unroll
         for (int t = 0; t < (MIRROR ? NA : 1); ++t) { aco[t][0] = 0.0; aco[t][1] = 0.0; }
       }
-      if (DOA_SCAN_PP) bar_sync(1 + wg);                         // my group's turn on the pipe
+      bar_sync(1 + wg);                         // my group's turn on the pipe
       if (gv) {
-        if (!MIRROR || DOA_SCAN_EO == 0) {
+        if (!MIRROR) {
 #pragma unroll
           for (int s = 0; s < S; ++s) {
             const double av = STREAM_A ? __ldg(cgc + s * 32) : a[STREAM_A ? 0 : s];
@@ -714,7 +597,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, DOA_SCAN_MINB) scan_cta_kernel
           }
         }
       }
-      if (DOA_SCAN_PP) bar_arrive(2 - wg);                       // hand the pipe to the other group
+      bar_arrive(2 - wg);                       // hand the pipe to the other group
       if (!gv) continue;
       if (!MIRROR) {
         long long fi[2 * NA];
@@ -739,18 +622,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, DOA_SCAN_MINB) scan_cta_kernel
       }
     }
   }
-  if (DOA_SCAN_PP && wg == 0) bar_sync(1);                       // consume the other group's last hand-off
-}
-
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
+  if (wg == 0) bar_sync(1);                       // consume the other group's last hand-off
 }
 
 template <int S, bool MIRROR>
@@ -758,13 +630,8 @@ cudaError_t launch_scan_cta(const doa_plan_s* p, int64_t B, float* P, cudaStream
   using Shape = ScanShape<S, MIRROR>;
   constexpr int NA = Shape::NA, W = Shape::W, NB = Shape::NB;
   const size_t smem = (size_t)NB * S * NA * 32 * sizeof(double);
-  static int occ = 0;
-  if (!occ) {
-    cudaFuncSetAttribute(scan_cta_kernel<S, false, MIRROR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(scan_cta_kernel<S, true, MIRROR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_cta_kernel<S, false, MIRROR>, kCtaWarps * 32, smem);
-    if (occ < 1) occ = 1;
-  }
+  const int occ = kernel_occupancy(scan_cta_kernel<S, false, MIRROR>, kCtaWarps * 32, smem);
+  if (P) kernel_occupancy(scan_cta_kernel<S, true, MIRROR>, kCtaWarps * 32, smem);   // sets its smem attribute
   const int64_t span = MIRROR ? (p->L + 1) / 2 : p->L;          // tile indices the blocks own
   const int64_t nwb = (span + (W - 2) - 1) / (W - 2);            // angle blocks owning [0, span)
   const int64_t gx = (nwb + NB - 1) / NB;                        // angle columns
@@ -833,50 +700,23 @@ cudaError_t launch_coef(const doa_plan_s* p, const double* lam, const double* V,
                         cudaStream_t s) {
   const int M = p->M;
   count_launch();
-  if (M <= 16 && DOA_COEF_MMA) {
+  if (M <= 16) {
     const size_t smem = (size_t)kCoefMmaWarps * 2 * kCoefMmaPlane * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(coef_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
-    static int occ = 0;
-    if (!occ) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, coef_mma_kernel, kCoefMmaWarps * 32, smem);
-      if (occ < 1) occ = 1;
-    }
+    const int occ = kernel_occupancy(coef_mma_kernel, kCoefMmaWarps * 32, smem);
     int64_t nb = (B + kCoefMmaWarps - 1) / kCoefMmaWarps;
-    const int64_t slots = (int64_t)sm_count() * occ * DOA_COEF_WAVES;
+    const int64_t slots = (int64_t)sm_count() * occ * kCoefWaves;
     if (nb > slots) nb = slots;
     coef_mma_kernel<<<(unsigned)nb, kCoefMmaWarps * 32, smem, s>>>(
         lam, reinterpret_cast<const double2*>(V), B, M, p->D, p->alg, p->coef, p->cnt, info);
     return cudaGetLastError();
   }
-  if (DOA_COEF_MMA) {
-    static bool attr_big = false;
-    if (!attr_big) {
-      cudaFuncSetAttribute(coef_big_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CoefBig<32>::SMEM);
-      cudaFuncSetAttribute(coef_big_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CoefBig<64>::SMEM);
-      attr_big = true;
-    }
-    auto go = [&](auto kern, size_t smem) {
-      kern<<<(unsigned)B, kCoefBigWarps * 32, smem, s>>>(lam, reinterpret_cast<const double2*>(V), B, M, p->D, p->alg,
-                                                         p->coef, p->cnt, info);
-    };
-    if (M <= 32) go(coef_big_kernel<32>, CoefBig<32>::SMEM);
-    else go(coef_big_kernel<64>, CoefBig<64>::SMEM);
-    return cudaGetLastError();
-  }
-  const int wpc = M <= 32 ? kCoefWarps : 2;
-  const size_t smem = (size_t)wpc * (M * (M + 1) + 32) * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(coef_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(2 * (kMaxM * (kMaxM + 1) + 32) * sizeof(double2)));
-    attr = true;
-  }
-  coef_kernel<<<(unsigned)((B + wpc - 1) / wpc), wpc * 32, smem, s>>>(lam, reinterpret_cast<const double2*>(V), B, M,
-                                                                       p->D, p->alg, p->coef, p->cnt, info);
+  auto go = [&](auto kern, size_t smem) {
+    kernel_occupancy(kern, kCoefBigWarps * 32, smem);                 // sets the smem attribute
+    kern<<<(unsigned)B, kCoefBigWarps * 32, smem, s>>>(lam, reinterpret_cast<const double2*>(V), B, M, p->D, p->alg,
+                                                       p->coef, p->cnt, info);
+  };
+  if (M <= 32) go(coef_big_kernel<32>, CoefBig<32>::SMEM);
+  else go(coef_big_kernel<64>, CoefBig<64>::SMEM);
   return cudaGetLastError();
 }
 

@@ -1,5 +1,8 @@
-"""Multi-process (world_size 2, gloo, CPU) tests of the frame-sharding / peak-gather host logic
-(paper_2007_14135_b200/dist.py) that bench.py runs over NCCL on GPUs."""
+"""Multi-process (world_size 2-3, gloo, CPU) tests of the frame-sharding / peak-gather host logic
+(paper_2007_14135_b200/dist.py) that bench.py runs over NCCL on GPUs.  The strong-scaling test
+shards a real batch with shard_range, lets every rank compute its shard's peak lists (with the
+oracle standing in for the GPU path, which needs a device), gathers them with gather_sharded and
+checks the result equals the single-process batch bitwise."""
 import os
 import socket
 
@@ -39,6 +42,61 @@ def _worker(rank, world, port, per_rank, D, q):
             q.put(out.clone())
     finally:
         dist.destroy_process_group()
+
+
+def _strong_worker(rank, world, port, total, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_2007_14135_b200 import dist as pd
+        from synth import get_config, generate
+        cfg = get_config("c4").with_(dtheta=0.5, N=64)
+        packs = []
+        frames = pd.shard_range(total, world, rank)
+        X = generate(cfg, frames=frames) if len(frames) else None
+        for alg in ("phd", "music", "ev", "mn"):
+            if X is None:
+                t = torch.zeros((0, 2 * cfg.D + 2), dtype=torch.int32)
+            else:
+                r = oracle.run_batch(alg, X, cfg.D, 0.5, cfg.theta0, cfg.dtheta, cfg.L)
+                t = pd.pack_peaks(torch.from_numpy(r["idx"]), torch.from_numpy(r["val"]),
+                                  torch.from_numpy(r["npk"]), torch.from_numpy(r["info"]))
+            packs.append(t)
+        out = pd.gather_sharded(torch.stack(packs), total)
+        if rank == 0:
+            q.put(out.clone())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total,world", [(13, 2), (13, 3), (2, 3)])
+def test_strong_sharded_gather_equals_single_batch(total, world):
+    """Contiguous shards of a c4-like batch (uneven when world does not divide it, including an
+    empty shard), each rank's peak lists computed on its shard only, gathered in frame order:
+    bitwise equal to the whole batch computed in one process."""
+    import oracle
+    from paper_2007_14135_b200 import dist as pd
+    from synth import get_config, generate
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_strong_worker, args=(r, world, port, total, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = get_config("c4").with_(dtheta=0.5, N=64)
+    X = generate(cfg, frames=range(total))
+    assert out.shape == (4, total, 2 * cfg.D + 2)
+    for a, alg in enumerate(("phd", "music", "ev", "mn")):
+        r = oracle.run_batch(alg, X, cfg.D, 0.5, cfg.theta0, cfg.dtheta, cfg.L)
+        ref = pd.pack_peaks(torch.from_numpy(r["idx"]), torch.from_numpy(r["val"]),
+                            torch.from_numpy(r["npk"]), torch.from_numpy(r["info"]))
+        assert torch.equal(out[a], ref), alg
 
 
 def test_weak_sharded_gather_equals_single_process():

@@ -223,3 +223,70 @@ def test_nonsymmetric_grid_is_plain(orc):
     q = np.einsum("ml,mn,nl->l", A.conj(), Cm, A).real
     f, _ = orc.spectrum("music", cfg.D, 0.5, lam, V, th0, dth, L)
     assert np.max(np.abs(f - q)) <= 1e3 * EPS * np.sum(np.abs(Cm)) * cfg.M
+
+
+# ------------------------------------------------------------------------------------------------
+# Pins of the two guard branches (Q12 and G1) against closed forms.
+
+def test_exact_zero_floor_and_fp32_saturation(orc):
+    """Q12: f is floored at 1e-300 and the fp32 P = 1/f saturates at FLT_MAX.  M = 2, one snapshot
+    x = (1, 1) (a noise-free source at broadside): R = [[1, 1], [1, 1]], the oracle's Jacobi gives
+    e_min = (c, -c) with c = 1/sqrt(2) exactly (tau = 0 -> t = 1, s = t c = c), so at theta = 0
+    (grid index 90 of -90:1:90) e_min^H a = c - c = 0 exactly: f = 0 -> 1e-300 -> P = FLT_MAX,
+    the unique peak, val = FLT_MAX.  Elsewhere f = |c (1 - e^{-j pi u})|^2 = 1 - cos(pi u)."""
+    X = np.array([[[1.0 + 0j, 1.0 + 0j]]], dtype=np.complex64)
+    fmax = np.finfo(np.float32).max
+    lam, V, _, _ = orc.eig(orc.covariance(X[0]))
+    assert lam[0] == 0.0 and V[0, 0] == -V[1, 0]
+    for alg in ("phd", "music"):                       # K = 1: the same C
+        f, info = orc.spectrum(alg, 1, 0.5, lam, V, -90.0, 1.0, 181)
+        assert f[90] == 1e-300                          # the floor (Q12), not 0
+        u = np.sin(np.deg2rad(_grid_theta(-90.0, 1.0, 181)))
+        ref = 1.0 - np.cos(np.pi * u)
+        m = np.abs(u) > 1e-3
+        assert np.max(np.abs(f[m] - ref[m]) / ref[m]) <= 1e-13
+        r = orc.run_batch(alg, X, 1, 0.5, -90.0, 1.0, 181, want_P=True)
+        assert r["P"][0, 90] == fmax                    # saturated, not inf
+        assert np.all(np.isfinite(r["P"][0]))
+        assert r["idx"][0, 0] == 90 and r["val"][0, 0] == fmax and r["npk"][0] == 1
+        np.testing.assert_allclose(r["P"][0, m], (1.0 / ref[m]).astype(np.float32), rtol=1e-6)
+
+
+def _v3(cols):
+    return np.ascontiguousarray(np.array(cols, dtype=np.complex128).T)   # columns -> V[i][j]
+
+
+def test_ev_degenerate_clamp_value(orc):
+    """G1 (EV): a noise eigenvalue <= 100 eps lambda_max is clamped to that floor, i.e. weight
+    1/(100 eps lambda_max), DEGENERATE; V = I makes |e_k^H a|^2 = 1, so f is the weight sum:
+    lambda = (1e-20, 0.5, 1), K = 2 -> f = 1/(100 eps) + 2.  With lambda_max <= 0 the floor is 0
+    and every weight is 1 -> f = K.  A clean spectrum (lambda = (0.25, 0.5, 1)) has no flag and
+    f = 4 + 2."""
+    V = np.eye(3, dtype=np.complex128)
+    f, info = orc.spectrum("ev", 1, 0.5, np.array([1e-20, 0.5, 1.0]), V, -90.0, 1.0, 181)
+    assert info & orc.INFO_DEGENERATE
+    np.testing.assert_allclose(f, 1.0 / (100 * EPS) + 2.0, rtol=1e-14)
+    f, info = orc.spectrum("ev", 1, 0.5, np.array([-1e-18, -1e-19, 0.0]), V, -90.0, 1.0, 181)
+    assert info & orc.INFO_DEGENERATE
+    np.testing.assert_allclose(f, 2.0, rtol=1e-14)
+    f, info = orc.spectrum("ev", 1, 0.5, np.array([0.25, 0.5, 1.0]), V, -90.0, 1.0, 181)
+    assert info == 0
+    np.testing.assert_allclose(f, 6.0, rtol=1e-14)
+
+
+def test_mn_degenerate_unnormalised(orc):
+    """G1 (MN): with e1^H P_n e1 <= 100 eps the vector w = P_n e1 is kept unnormalised.  Noise
+    vectors (delta, s, 0) and (0, 0, 1), s = sqrt(1 - delta^2), signal (s, -delta, 0): P_n e1 =
+    delta (delta, s, 0), p0 = delta^2 = 1e-18 -> DEGENERATE and
+    f = |w^H a|^2 = delta^2 (1 + 2 delta s cos(pi u))  (normalising would give f / delta^4).
+    Above the threshold (delta = 0.3) w is normalised: f = (1 + 2 delta s cos(pi u)) / delta^2."""
+    th = _grid_theta(-90.0, 1.0, 181)
+    u = np.sin(np.deg2rad(th))
+    for delta, degen in ((1e-9, True), (0.3, False)):
+        s = np.sqrt(1.0 - delta * delta)
+        V = _v3([[delta, s, 0.0], [0.0, 0.0, 1.0], [s, -delta, 0.0]])
+        f, info = orc.spectrum("mn", 1, 0.5, np.array([0.1, 0.2, 3.0]), V, -90.0, 1.0, 181)
+        base = 1.0 + 2.0 * delta * s * np.cos(np.pi * u)
+        ref = delta ** 2 * base if degen else base / delta ** 2
+        assert bool(info & orc.INFO_DEGENERATE) == degen
+        np.testing.assert_allclose(f, ref, rtol=1e-12)

@@ -12,9 +12,41 @@ delta is a certified tie and either outcome is accepted.
 """
 from __future__ import annotations
 
+import json
+import os
+
 import numpy as np
 
 EPS = np.finfo(float).eps
+
+# Tie accounting ("report the count of certified ties").  Every (frame, algorithm)
+# decision list a GPU test compares is recorded under the running test's id: identical to the
+# oracle, or accepted through certified ties (with their count).  conftest.py writes the table to
+# gpurun_out/parity_ties.json and prints it at the end of the session.
+TIE_LOG: dict = {}
+CURRENT = {"test": "?"}
+
+
+def record(ties: int, exact: bool):
+    e = TIE_LOG.setdefault(CURRENT["test"], {"frame_algs": 0, "exact": 0, "with_certified_ties": 0,
+                                             "certified_ties": 0})
+    e["frame_algs"] += 1
+    if exact:
+        e["exact"] += 1
+    else:
+        e["with_certified_ties"] += 1
+        e["certified_ties"] += ties
+
+
+def dump(path: str):
+    if not TIE_LOG:
+        return None
+    tot = {k: sum(v[k] for v in TIE_LOG.values()) for k in ("frame_algs", "exact", "with_certified_ties",
+                                                             "certified_ties")}
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    with open(path, "w") as fh:
+        json.dump({"total": tot, "tests": TIE_LOG}, fh, indent=1, sort_keys=True)
+    return tot
 
 
 def toeplitz_sums(Cm: np.ndarray) -> np.ndarray:
@@ -40,6 +72,13 @@ def _rel(a, b):
 
 def certify(gpu_idx, orc_idx, f: np.ndarray, delta: np.ndarray, D: int):
     """Return (ok, n_certified_ties, reason).  gpu_idx/orc_idx: length-D arrays (-1 padded)."""
+    ok, ties, why = _certify(gpu_idx, orc_idx, f, delta, D)
+    if ok:
+        record(ties, ties == 0 and [int(i) for i in gpu_idx if i >= 0] == [int(i) for i in orc_idx if i >= 0])
+    return ok, ties, why
+
+
+def _certify(gpu_idx, orc_idx, f, delta, D):
     g = [int(i) for i in gpu_idx if i >= 0]
     o = [int(i) for i in orc_idx if i >= 0]
     if g == o:
