@@ -229,31 +229,29 @@ class Workload:
         self.spec_ev = []
 
     def compute(self, sh, stream=None, record=False):
-        """S1-S7 for the four estimators on stream handle `sh` + packing of the peak lists;
-        returns the number of libdoa kernel launches."""
+        """S1-S7 for the four estimators (doa_run_multi: covariance + eig once, then per plan the
+        coefficients, scan and peak selection) + packing of the peak lists; returns the number of
+        libdoa kernel launches.  record=True additionally times each plan's doa_spectrum (the scan's
+        coefficient + contraction kernels) on the eigenpairs of the step, for the roofline."""
         import torch
         from paper_2007_14135_b200 import binding as bd
         from paper_2007_14135_b200 import dist as pdist
-        n = 0
         if self.B == 0:
             return 0
-        bd.doa_covariance(self.plans[0].h, self.X, self.R, sh)
-        n += bd.doa_last_launch_count()
-        bd.doa_eig(self.plans[0].h, self.R, self.lam, self.V, self.info_eig, sh)
-        n += bd.doa_last_launch_count()
-        for a, p in enumerate(self.plans):
-            self.info[a].copy_(self.info_eig)
-            if record:
+        hs = [p.h for p in self.plans]
+        bd.doa_run_multi(hs, self.X, self.idx, self.val, self.npk, self.info, sh)
+        n = bd.doa_last_launch_count()
+        if record:
+            bd.doa_covariance(hs[0], self.X, self.R, sh)
+            bd.doa_eig(hs[0], self.R, self.lam, self.V, self.info_eig, sh)
+            for a, h in enumerate(hs):
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-            bd.doa_spectrum(p.h, self.lam, self.V, self.info[a], None, sh)
-            n += bd.doa_last_launch_count()
-            if record:
+                bd.doa_spectrum(h, self.lam, self.V, self.info_eig, None, sh)
                 e1.record(stream)
                 self.spec_ev.append((e0, e1))
-            bd.doa_peaks(p.h, self.B, self.idx[a], self.val[a], self.npk[a], self.info[a], sh)
-            n += bd.doa_last_launch_count()
+            bd.doa_run_multi(hs, self.X, self.idx, self.val, self.npk, self.info, sh)   # restore the outputs
         pdist.pack_peaks(self.idx, self.val, self.npk, self.info, out=self.packed)
         return n
 
@@ -271,10 +269,10 @@ def timed_steps(args, wl, ws, dev, stream, use_graph, gather):
         gather(wl)
     torch.cuda.synchronize()
     graph, per = None, 0
+    for _ in range(min(args.steps, 5)):               # per-launch timing of doa_spectrum, outside the timed steps
+        wl.compute(s, stream, record=True)
+    torch.cuda.synchronize()
     if use_graph:
-        for _ in range(min(args.steps, 5)):           # per-launch timing of doa_spectrum, outside the graph
-            wl.compute(s, stream, record=True)
-        torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
             per = wl.compute(stream.cuda_stream)
@@ -297,7 +295,7 @@ def timed_steps(args, wl, ws, dev, stream, use_graph, gather):
             graph.replay()
             launches += per
         else:
-            launches += wl.compute(s, stream, record=True)
+            launches += wl.compute(s, stream)
         gather(wl)
     ev1.record(stream)
     torch.cuda.synchronize()

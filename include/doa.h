@@ -136,7 +136,9 @@ doa_status_t doa_eig(doa_plan_t plan, const double* R, int64_t B, double* lambda
  * u_i = 2 (d/lambda) sin(theta_i), floored at 1e-300 (Q12), and local-maximum candidate
  * detection (Step-6 findPeaks; Q9/Q10) into the plan's candidate lists.
  * lambda/V as produced by doa_eig.  P: NULL, or float [B][L] receiving 1/f_i (fp32, saturating).
- * info[b] |= DEGENERATE where applicable. */
+ * info[b] |= DEGENERATE where applicable.  Batches of B > 16 frames run the scan as an FP64
+ * tensor-core (DMMA) contraction; B <= 16 runs the direct scan (steering generated once per angle
+ * in registers, csrc/scan_direct.cu), which rounds differently (both within the parity bars). */
 doa_status_t doa_spectrum(doa_plan_t plan, const double* lambda, const double* V, int64_t B,
                           float* P, int32_t* info, doa_stream_t stream);
 
@@ -153,6 +155,22 @@ doa_status_t doa_peaks(doa_plan_t plan, int64_t B, int32_t* idx, float* val, int
  * synchronises the device once). */
 doa_status_t doa_run(doa_plan_t plan, const float* X, int64_t B, int64_t N, int32_t* idx,
                      float* val, int32_t* npk, float* P, int32_t* info, doa_stream_t stream);
+
+/* S1-S7 for several plans on one batch, device buffers: nplans >= 1 distinct plans that share M
+ * and D (typically PHD, MUSIC, EV and MN on one grid).  X as doa_covariance; the covariance and
+ * the eigendecomposition run once (in plans[0]'s scratch), then every plan's S3-S7; outputs per
+ * plan a: idx int32 [nplans][B][D], val float [nplans][B][D], npk int32 [nplans][B], info int32
+ * [nplans][B] (overwritten), all device pointers.  For small batches (B <= 16) plans that share
+ * the grid (M, d/lambda, theta0, dtheta, L) are evaluated by ONE direct scan launch that generates
+ * the steering once per angle for all of them (csrc/scan_direct.cu) — the non-tensor-core path
+ * for single frames; larger batches use the FP64 tensor-core (DMMA) contraction per plan.  The
+ * two paths round differently (both within the parity bars), so a frame's P can differ in the
+ * last bits between a batch of <= 16 and a larger one.  Per-plan candidate lists are left for
+ * doa_peaks as after doa_spectrum.  Errors as doa_run; the plans must be distinct, created on the
+ * current device, with max_batch >= B. */
+doa_status_t doa_run_multi(const doa_plan_t* plans, int32_t nplans, const float* X, int64_t B,
+                           int64_t N, int32_t* idx, float* val, int32_t* npk, int32_t* info,
+                           doa_stream_t stream);
 
 /* End-to-end variant of doa_run with HOST buffers, for nplans >= 1 plans that share M and D
  * (typically the four estimators): X_host complex64 [B][N][M] is copied host->device in chunks

@@ -21,7 +21,7 @@ STATUS = {0: "DOA_OK", 1: "DOA_ERR_INVALID_ARG", 2: "DOA_ERR_UNSUPPORTED", 3: "D
 
 EXPORTS = ("doa_generate", "doa_plan_create", "doa_plan_create_array", "doa_plan_destroy", "doa_plan_capacity",
            "doa_plan_info", "doa_covariance", "doa_eig",
-           "doa_spectrum", "doa_peaks", "doa_run", "doa_run_host", "doa_last_launch_count",
+           "doa_spectrum", "doa_peaks", "doa_run", "doa_run_multi", "doa_run_host", "doa_last_launch_count",
            "doa_status_string", "doa_last_error", "doa_version")
 
 
@@ -55,6 +55,7 @@ def _load():
     L.doa_peaks.argtypes = [vp, i64, i32p, fp, i32p, i32p, vp]
     L.doa_run.argtypes = [vp, fp, i64, i64, i32p, fp, i32p, fp, i32p, vp]
     L.doa_run_host.argtypes = [C.POINTER(C.c_void_p), i32, fp, i64, i64, i32p, fp, i32p, i32p, vp]
+    L.doa_run_multi.argtypes = [C.POINTER(C.c_void_p), i32, fp, i64, i64, i32p, fp, i32p, i32p, vp]
     L.doa_generate.argtypes = [i32, d, i32, dp, i32, d, C.c_uint64, i64, i64, i64, fp, vp]
     L.doa_last_launch_count.restype = i32
     L.doa_status_string.argtypes = [C.c_int]
@@ -245,6 +246,38 @@ def doa_run(plan, X, idx, val, npk, info, P=None, stream=None):
         _need_P(P, B, pi)
     _check(lib.doa_run(plan, _ptr(_f32(X)), B, N, _ptr(idx), _ptr(val), _ptr(npk), _ptr(P), _ptr(info),
                        _stream(stream)))
+
+
+def doa_run_multi(plans, X, idx, val, npk, info, stream=None):
+    """Several plans (sharing M, D) on one device batch: X complex64 (B, N, M); outputs on the
+    device, idx/val (nplans, B, D), npk/info (nplans, B)."""
+    if not isinstance(plans, (list, tuple)):
+        plans = [plans]
+    pi = plan_info(plans[0])
+    n = len(plans)
+    _need(X, "X", torch.complex64, (None, None, pi.M), pi.device)
+    B, N = X.shape[0], X.shape[1]
+    _need(idx, "idx", torch.int32, (n, B, pi.D), pi.device)
+    _need(val, "val", torch.float32, (n, B, pi.D), pi.device)
+    _need(npk, "npk", torch.int32, (n, B), pi.device)
+    _need(info, "info", torch.int32, (n, B), pi.device)
+    arr = (C.c_void_p * n)(*[_hval(p) for p in plans])
+    _check(lib.doa_run_multi(arr, n, _ptr(_f32(X)), B, N, _ptr(idx), _ptr(val), _ptr(npk), _ptr(info),
+                             _stream(stream)))
+
+
+def run_multi(plans, X, stream=None):
+    """Convenience: all `plans` (Plan objects sharing M, D, device) on X -> (idx, val, npk, info)
+    device tensors of shape (nplans, B, D) / (nplans, B)."""
+    dev = plans[0].device
+    B, n, D = X.shape[0], len(plans), plans[0].D
+    idx = torch.empty((n, B, D), dtype=torch.int32, device=dev)
+    val = torch.empty((n, B, D), dtype=torch.float32, device=dev)
+    npk = torch.empty((n, B), dtype=torch.int32, device=dev)
+    info = torch.empty((n, B), dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        doa_run_multi([p.h for p in plans], X, idx, val, npk, info, stream)
+    return idx, val, npk, info
 
 
 def doa_run_host(plans, X_host, idx, val, npk, info, stream=None):

@@ -81,6 +81,82 @@ cudaError_t spectrum_stage(const doa_plan_s* p, const double* lam, const double*
   return doa::launch_scan(p, B, P, s);
 }
 
+// S1-S7 for nplans plans sharing M and D on device buffers (doa_run_multi, and doa_run_host per
+// chunk): covariance and eigendecomposition once (plans[0]'s scratch), then per plan the
+// coefficients, the scan — for small batches the direct scan, one launch per group of up to four
+// plans that share the grid — and the peak selection.  Plan a's outputs live at idx + a*ldo*D,
+// val + a*ldo*D, npk + a*ldo, info + a*ldo.
+cudaError_t run_plans(doa_plan_s* const* plans, int nplans, const float* X, int64_t B, int64_t N, int32_t* idx,
+                      float* val, int32_t* npk, int32_t* info, int64_t ldo, cudaStream_t st,
+                      cudaEvent_t x_consumed = nullptr) {
+  doa_plan_s* p = plans[0];
+  const int M = p->M, D = p->D;
+  cudaError_t e = doa::launch_covariance(X, B, N, M, p->R, st);
+  if (e == cudaSuccess && x_consumed) e = cudaEventRecord(x_consumed, st);   // X no longer needed
+  if (e == cudaSuccess) e = doa::launch_eig(p->R, B, M, p->lam, p->V, info, st);
+  for (int a = 1; a < nplans && e == cudaSuccess; ++a)        // every plan starts from the eig flags
+    e = cudaMemcpyAsync(info + (size_t)a * ldo, info, (size_t)B * sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
+  {                                                   // S3: one coefficient launch for the ULA plans
+    const doa_plan_s* ula[64];
+    int32_t* ula_info[64];
+    int nu = 0;
+    for (int a = 0; a < nplans && e == cudaSuccess; ++a) {
+      doa_plan_s* q = plans[a];
+      if (q->geom == 1) e = doa::launch_array_spectrum(q, p->lam, p->V, B, nullptr, info + (size_t)a * ldo, st);
+      else if (nu < 64) { ula[nu] = q; ula_info[nu++] = info + (size_t)a * ldo; }
+      else e = doa::launch_coef(q, p->lam, p->V, B, info + (size_t)a * ldo, st);
+    }
+    if (e == cudaSuccess && nu) e = doa::launch_coef_multi(ula, nu, p->lam, p->V, B, ula_info, st);
+  }
+  for (int a = 0; a < nplans && e == cudaSuccess;) {
+    doa_plan_s* q = plans[a];
+    if (q->geom == 1) { ++a; continue; }
+    if (B > doa::kDirectMaxB) { e = doa::launch_scan(q, B, nullptr, st); ++a; continue; }
+    doa::DirectScanArgs da = {};
+    int n = 0;
+    while (a < nplans && n < doa::kMaxDirectPlans && doa::direct_compatible(q, plans[a])) {
+      doa_plan_s* r = plans[a++];
+      da.coef[n] = r->coef; da.cnt[n] = r->cnt; da.cidx[n] = r->cand_idx; da.cf[n] = r->cand_f; da.P[n] = nullptr;
+      ++n;
+    }
+    da.nplans = n;
+    e = doa::launch_scan_direct(da, q, B, st);
+  }
+  for (int a0 = 0; a0 < nplans && e == cudaSuccess; a0 += 4) {     // S7: one launch per 4 plans
+    doa::SelectPlans sp = {};
+    sp.nplans = nplans - a0 < 4 ? nplans - a0 : 4;
+    for (int k = 0; k < sp.nplans; ++k) {
+      doa_plan_s* q = plans[a0 + k];
+      const size_t a = (size_t)(a0 + k);
+      sp.cnt[k] = q->cnt; sp.cidx[k] = q->cand_idx; sp.cf[k] = q->cand_f; sp.cap[k] = q->cap;
+      sp.idx[k] = idx + a * ldo * D; sp.val[k] = val + a * ldo * D; sp.npk[k] = npk + a * ldo;
+      sp.info[k] = info + a * ldo;
+      q->last_B = B;
+    }
+    e = doa::launch_select_multi(sp, D, B, st);
+  }
+  return e;
+}
+
+doa_status_t check_plan_set(const char* fn, const doa_plan_t* plans, int32_t nplans, int64_t B) {
+  if (!plans || nplans < 1) return fail(DOA_ERR_INVALID_ARG, "%s: need nplans >= 1 plans", fn);
+  const int dev = doa::current_device();
+  for (int k = 0; k < nplans; ++k) {
+    if (!plans[k]) return fail(DOA_ERR_INVALID_ARG, "%s: plans[%d] is NULL", fn, k);
+    if (plans[k]->device != dev)
+      return fail(DOA_ERR_INVALID_ARG, "%s: plans[%d] was created on device %d, current device is %d", fn, k,
+                  plans[k]->device, dev);
+    if (plans[k]->M != plans[0]->M || plans[k]->D != plans[0]->D)
+      return fail(DOA_ERR_INVALID_ARG, "%s: plans must share M and D", fn);
+    if (B < 0 || B > plans[k]->max_batch)
+      return fail(DOA_ERR_INVALID_ARG, "%s: B=%lld outside [0, max_batch=%lld] of plans[%d]", fn, (long long)B,
+                  (long long)plans[k]->max_batch, k);
+    for (int j = 0; j < k; ++j)
+      if (plans[j] == plans[k]) return fail(DOA_ERR_INVALID_ARG, "%s: plans[%d] repeats plans[%d]", fn, k, j);
+  }
+  return DOA_OK;
+}
+
 }  // namespace
 
 namespace doa {
@@ -341,18 +417,29 @@ doa_status_t doa_run(doa_plan_t p, const float* X, int64_t B, int64_t N, int32_t
   return DOA_OK;
 }
 
+doa_status_t doa_run_multi(const doa_plan_t* plans, int32_t nplans, const float* X, int64_t B, int64_t N,
+                           int32_t* idx, float* val, int32_t* npk, int32_t* info, doa_stream_t s) {
+  g_launches = 0;
+  const doa_status_t st = check_plan_set("doa_run_multi", plans, nplans, B);
+  if (st != DOA_OK) return st;
+  if (N < 1) return fail(DOA_ERR_INVALID_ARG, "doa_run_multi: N=%lld < 1", (long long)N);
+  if (B == 0) return DOA_OK;
+  DOA_CHECK_PTR(X, 8);
+  DOA_CHECK_PTR(idx, 4);
+  DOA_CHECK_PTR(val, 4);
+  DOA_CHECK_PTR(npk, 4);
+  DOA_CHECK_PTR(info, 4);
+  DOA_TRY(ensure_run_scratch(plans[0]), "doa_run_multi: scratch allocation");
+  DOA_TRY(run_plans(plans, nplans, X, B, N, idx, val, npk, info, B, (cudaStream_t)s), "doa_run_multi");
+  return DOA_OK;
+}
+
 doa_status_t doa_run_host(const doa_plan_t* plans, int32_t nplans, const float* X_host, int64_t B, int64_t N,
                           int32_t* idx_host, float* val_host, int32_t* npk_host, int32_t* info_host,
                           doa_stream_t s) {
-  if (!plans || nplans < 1) return fail(DOA_ERR_INVALID_ARG, "doa_run_host: need nplans >= 1 plans");
-  for (int k = 0; k < nplans; ++k) {
-    if (!plans[k]) return fail(DOA_ERR_INVALID_ARG, "doa_run_host: plans[%d] is NULL", k);
-    if (plans[k]->device != doa::current_device())
-      return fail(DOA_ERR_INVALID_ARG, "doa_run_host: plans[%d] was created on device %d, current device is %d", k,
-                  plans[k]->device, doa::current_device());
-    if (plans[k]->M != plans[0]->M || plans[k]->D != plans[0]->D)
-      return fail(DOA_ERR_INVALID_ARG, "doa_run_host: plans must share M and D");
-    DOA_CHECK_B(plans[k], B);
+  {
+    const doa_status_t st0 = check_plan_set("doa_run_host", plans, nplans, B);
+    if (st0 != DOA_OK) return st0;
   }
   doa_plan_s* p = plans[0];
   if (N < 1) return fail(DOA_ERR_INVALID_ARG, "doa_run_host: N=%lld < 1", (long long)N);
@@ -408,23 +495,11 @@ doa_status_t doa_run_host(const doa_plan_t* plans, int32_t nplans, const float* 
     DOA_TRY(cudaEventRecord(p->ev_copied[k], p->copy_stream), "doa_run_host: record");
     DOA_TRY(cudaStreamWaitEvent(st, p->ev_copied[k], 0), "doa_run_host: wait");
     g_launches = 0;
-    int32_t* info0 = d_info + b0;                   // plan 0's info slice holds eig flags first
-    DOA_TRY(doa::launch_covariance(p->dX[k], nb, N, M, p->R, st), "doa_run_host/covariance");
-    DOA_TRY(doa::launch_eig(p->R, nb, M, p->lam, p->V, info0, st), "doa_run_host/eig");
-    DOA_TRY(cudaEventRecord(p->ev_used[k], st), "doa_run_host: record");
-    for (int a = 1; a < nplans; ++a)   // every plan starts from the eigensolver's flags
-      DOA_TRY(cudaMemcpyAsync(d_info + (size_t)a * B + b0, info0, (size_t)nb * sizeof(int32_t),
-                              cudaMemcpyDeviceToDevice, st), "doa_run_host: info");
-    for (int a = 0; a < nplans; ++a) {
-      doa_plan_s* q = plans[a];
-      int32_t* inf = d_info + (size_t)a * B + b0;
-      DOA_TRY(spectrum_stage(q, p->lam, p->V, nb, nullptr, inf, st), "doa_run_host/spectrum");
-      DOA_TRY(doa::launch_select(q, nb, d_idx + ((size_t)a * B + b0) * D, d_val + ((size_t)a * B + b0) * D,
-                                 d_npk + (size_t)a * B + b0, inf, st), "doa_run_host/select");
-      q->last_B = 0;
-    }
+    DOA_TRY(run_plans(plans, nplans, p->dX[k], nb, N, d_idx + (size_t)b0 * D, d_val + (size_t)b0 * D, d_npk + b0,
+                      d_info + b0, B, st, p->ev_used[k]), "doa_run_host/run");
     launches += g_launches;
   }
+  for (int a = 0; a < nplans; ++a) plans[a]->last_B = 0;
   const size_t nBD = (size_t)nplans * B * D, nB = (size_t)nplans * B;
   DOA_TRY(cudaMemcpyAsync(idx_host, d_idx, nBD * sizeof(int32_t), cudaMemcpyDeviceToHost, st), "D2H");
   DOA_TRY(cudaMemcpyAsync(val_host, d_val, nBD * sizeof(float), cudaMemcpyDeviceToHost, st), "D2H");

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cfloat>
 #include <cstdint>
 
 #include "../../include/doa.h"
@@ -34,6 +35,31 @@ __host__ __device__ inline size_t coef_index(int64_t b, int j, int S) {
   return ((size_t)(b >> 3) * S + (j >> 2)) * 32 + (size_t)(b & 7) * 4 + (j & 3);
 }
 inline size_t coef_words(int64_t max_batch, int M) { return (size_t)((max_batch + 7) / 8) * ksteps(M) * 32; }
+
+// Q12: P = 1/f reported in fp32, saturating at FLT_MAX.
+__device__ __forceinline__ float to_p32(double f) {
+  const double p = 1.0 / f;
+  return p > (double)FLT_MAX ? FLT_MAX : (float)p;
+}
+// Floor and peak tests run on the IEEE bit patterns: for positive doubles they order like the
+// values (integer compares keep the FP64 pipe free).
+constexpr long long kInfBits = 0x7FF0000000000000LL;        // bits of +inf
+constexpr long long kFloorBits = 0x01A56E1FC2F8F359LL;      // bits of 1e-300 (kFloor, Q12)
+// max(f, 1e-300) with NaN, +-0 and negative values -> 1e-300 (the oracle's floor), on the bits
+__device__ __forceinline__ long long floor_bits(long long x) {
+  x = x > kInfBits ? kFloorBits : x;
+  return x > kFloorBits ? x : kFloorBits;
+}
+
+// Grid angle (Q8, Q26): theta_i = theta0 + i dtheta (rounded multiply, then rounded add); on a
+// symmetric grid the upper half i >= ceil(L/2) is built from the other end, -theta_{L-1-i}.
+// u = 2 (d/lambda) sin(theta) with sinpi, odd in theta, so mirrored angles give u exactly negated.
+__device__ __forceinline__ double grid_u(int64_t i, double theta0, double dtheta, double dl, int L, bool sym) {
+  double th;
+  if (sym && i >= (L + 1) / 2) th = -__dadd_rn(__dmul_rn((double)(L - 1 - i), dtheta), theta0);
+  else th = __dadd_rn(__dmul_rn((double)i, dtheta), theta0);
+  return 2.0 * dl * sinpi(th / 180.0);
+}
 
 }  // namespace doa
 
@@ -78,9 +104,50 @@ cudaError_t launch_covariance(const float* X, int64_t B, int64_t N, int M, doubl
 cudaError_t launch_eig(const double* R, int64_t B, int M, double* lam, double* V, int32_t* info, cudaStream_t s);
 cudaError_t launch_coef(const doa_plan_s* p, const double* lam, const double* V, int64_t B, int32_t* info,
                         cudaStream_t s);
+// S3 for several plans sharing M, D from one set of eigenpairs (one launch for M <= 16)
+constexpr int kMaxCoefPlans = 4;
+struct CoefPlans {
+  int alg[kMaxCoefPlans];
+  double* coef[kMaxCoefPlans];
+  int32_t* cnt[kMaxCoefPlans];
+  int32_t* info[kMaxCoefPlans];
+  int nplans;
+};
+cudaError_t launch_coef_multi(const doa_plan_s* const* plans, int nplans, const double* lam, const double* V,
+                              int64_t B, int32_t* const* info, cudaStream_t s);
 cudaError_t launch_scan(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s);
 cudaError_t launch_select(const doa_plan_s* p, int64_t B, int32_t* idx, float* val, int32_t* npk, int32_t* info,
                           cudaStream_t s);
+// S7 for up to kMaxCoefPlans plans sharing D in one launch
+struct SelectPlans {
+  const int32_t* cnt[4];
+  const int32_t* cidx[4];
+  const double* cf[4];
+  int cap[4];
+  int32_t* idx[4];
+  float* val[4];
+  int32_t* npk[4];
+  int32_t* info[4];
+  int nplans;
+};
+cudaError_t launch_select_multi(const SelectPlans& sp, int D, int64_t B, cudaStream_t s);
+// Direct (non-tensor-core) scan for small batches (csrc/scan_direct.cu): one launch evaluates up to
+// kMaxDirectPlans ULA plans that share M, d/lambda and the grid (e.g. the four estimators of a
+// frame), steering generated once per angle.  `p` supplies the shared parameters; the plans'
+// coefficients must be in place (launch_coef) and their candidate counters zeroed.
+constexpr int kMaxDirectPlans = 4;
+constexpr int64_t kDirectMaxB = 16;      // batches up to this size take the direct scan
+struct DirectScanArgs {
+  const double* coef[kMaxDirectPlans];
+  int32_t* cnt[kMaxDirectPlans];
+  int32_t* cidx[kMaxDirectPlans];
+  double* cf[kMaxDirectPlans];
+  float* P[kMaxDirectPlans];
+  int nplans;
+};
+cudaError_t launch_scan_direct(const DirectScanArgs& args, const doa_plan_s* p, int64_t B, cudaStream_t s);
+// plans that may share one direct scan launch (same M, d/lambda, grid; ULA)
+bool direct_compatible(const doa_plan_s* a, const doa_plan_s* b);
 // general-array plans (csrc/array.cu): coefficients, scan into fbuf, 2-D candidates (+ optional P)
 cudaError_t launch_array_spectrum(const doa_plan_s* p, const double* lam, const double* V, int64_t B, float* P,
                                   int32_t* info, cudaStream_t s);

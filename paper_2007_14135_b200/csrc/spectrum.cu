@@ -17,10 +17,6 @@
 namespace doa {
 namespace {
 
-__device__ __forceinline__ float to_p32(double f) {
-  const double p = 1.0 / f;
-  return p > (double)FLT_MAX ? FLT_MAX : (float)p;      // Q12: fp32 P saturates at FLT_MAX
-}
 
 // T_j(psi) in the split layout of doa_internal.cuh: j = 0 -> 1; 1..M-1 -> cos(j psi);
 // JE..JE+M-2 -> sin((j-JE+1) psi) with JE = 4 ceil(M/4); else 0.
@@ -32,16 +28,6 @@ __device__ __forceinline__ double table_entry(int j, int M, double u) {
   if (j < M) return cospi((double)j * u);
   if (j >= JE && j < JE + M - 1) return sinpi((double)(j - JE + 1) * u);
   return 0.0;
-}
-
-// Grid angle (Q8, Q26): theta_i = theta0 + i dtheta (rounded multiply, then rounded add); on a
-// symmetric grid the upper half i >= ceil(L/2) is built from the other end, -theta_{L-1-i}.
-// u = 2 (d/lambda) sin(theta) with sinpi, odd in theta, so mirrored angles give u exactly negated.
-__device__ __forceinline__ double grid_u(int64_t i, double theta0, double dtheta, double dl, int L, bool sym) {
-  double th;
-  if (sym && i >= (L + 1) / 2) th = -__dadd_rn(__dmul_rn((double)(L - 1 - i), dtheta), theta0);
-  else th = __dadd_rn(__dmul_rn((double)i, dtheta), theta0);
-  return 2.0 * dl * sinpi(th / 180.0);
 }
 
 // Named barriers over the CTA's 256 threads (id 0 is __syncthreads): bar_sync waits until the
@@ -85,44 +71,16 @@ constexpr int kCoefMmaWarps = 8;
 constexpr int kCoefMmaLd = 20;                         // plane row stride (doubles), = 4 mod 16: conflict-free fragments
 constexpr int kCoefMmaPlane = 16 * kCoefMmaLd;         // doubles per plane
 
-__global__ void __launch_bounds__(kCoefMmaWarps * 32) coef_mma_kernel(const double* __restrict__ lam,
-                                                                      const double2* __restrict__ V, int64_t B,
-                                                                      int M, int D, int alg, double* __restrict__ coef,
-                                                                      int32_t* __restrict__ cnt,
-                                                                      int32_t* __restrict__ info) {
+// One frame's S3 by one warp.  Ure/Uim: the warp's planes holding the frame's eigenvectors
+// u_j[p] at j * ld + p (ascending j, zero outside j < K, p < M, up to 16 x 16); they are
+// overwritten (MN: vector 0 <- w; then the C tiles).  lb: the frame's ascending eigenvalues.
+__device__ __forceinline__ void coef_frame_mma(int lane, double* Ure, double* Uim, const double* lb, int M, int D,
+                                               int alg, double* __restrict__ coef, int64_t b,
+                                               int32_t* __restrict__ cnt, int32_t* __restrict__ info) {
   constexpr int ld = kCoefMmaLd;
-  extern __shared__ double cmsm[];                     // per warp: Ure, Uim planes; later C_re, C_im
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* Ure = cmsm + (size_t)warp * 2 * kCoefMmaPlane;
-  double* Uim = Ure + kCoefMmaPlane;
   const int S = ksteps(M);
   const int K = M - D;
-  const int nload = (alg == DOA_ALG_PHD) ? 1 : K;      // columns needed
-  // persistent warps: frame b, then b + stride, ...; the next frame's V loads are issued before
-  // the current frame is processed, so their latency overlaps the work
-  const int64_t stride = (int64_t)gridDim.x * kCoefMmaWarps;
-  int64_t b = (int64_t)blockIdx.x * kCoefMmaWarps + warp;
-  double2 tv[8];                                       // the whole 16 x 16 (j, p) slot grid, zero outside
-  auto load_v = [&](int64_t bb) {
-    const double2* Vb = V + (size_t)bb * M * M;
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int e = lane + 32 * r, pp = e & 15, j = e >> 4;
-      tv[r] = (bb < B && pp < M && j < nload) ? __ldg(Vb + pp * M + j) : make_double2(0.0, 0.0);
-    }
-  };
-  load_v(b);
-  for (; b < B; b += stride) {
-  const double* lb = lam + (size_t)b * M;
   int flag = 0;
-#pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    const int e = lane + 32 * r, pp = e & 15, j = e >> 4;
-    Ure[j * ld + pp] = tv[r].x;
-    Uim[j * ld + pp] = tv[r].y;
-  }
-  load_v(b + stride);
-  __syncwarp();
   int nv = (alg == DOA_ALG_MUSIC || alg == DOA_ALG_EV) ? K : 1;
   // EV weights w_j = 1/lambda_j (Q1), clamped at 100 eps lambda_max (DEGENERATE)
   double wj[4] = {1.0, 1.0, 1.0, 1.0};                 // weight of row j = 4J + lane%4 of X
@@ -227,6 +185,49 @@ __global__ void __launch_bounds__(kCoefMmaWarps * 32) coef_mma_kernel(const doub
     if (info && flag) info[b] |= flag;           // no read-modify-write round trip when clean
   }
   __syncwarp();                                        // C planes are read above before the next stores
+}
+
+// S3 for up to kMaxCoefPlans plans sharing M and D from the same eigenpairs (e.g. the four
+// estimators): each frame's eigenvectors are read from HBM once, then every plan's coefficients
+// are produced from them in turn by the warp (coef_frame_mma).  Persistent warps: frame b, then
+// b + stride, ...; the next frame's V loads are issued before the current frame is processed.
+__global__ void __launch_bounds__(kCoefMmaWarps * 32) coef_mma_kernel(const double* __restrict__ lam,
+                                                                      const double2* __restrict__ V, int64_t B,
+                                                                      int M, int D, CoefPlans cp) {
+  constexpr int ld = kCoefMmaLd;
+  extern __shared__ double cmsm[];                     // per warp: Ure, Uim planes; later C_re, C_im
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* Ure = cmsm + (size_t)warp * 2 * kCoefMmaPlane;
+  double* Uim = Ure + kCoefMmaPlane;
+  const int K = M - D;
+  bool only_phd = true;
+  for (int a = 0; a < cp.nplans; ++a) only_phd &= cp.alg[a] == DOA_ALG_PHD;
+  const int nload = only_phd ? 1 : K;                  // eigenvector columns needed
+  const int64_t stride = (int64_t)gridDim.x * kCoefMmaWarps;
+  int64_t b = (int64_t)blockIdx.x * kCoefMmaWarps + warp;
+  double2 tv[8];                                       // the whole 16 x 16 (j, p) slot grid, zero outside
+  auto load_v = [&](int64_t bb) {
+    const double2* Vb = V + (size_t)bb * M * M;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int e = lane + 32 * r, pp = e & 15, j = e >> 4;
+      tv[r] = (bb < B && pp < M && j < nload) ? __ldg(Vb + pp * M + j) : make_double2(0.0, 0.0);
+    }
+  };
+  load_v(b);
+  for (; b < B; b += stride) {
+    const double2 cur[8] = {tv[0], tv[1], tv[2], tv[3], tv[4], tv[5], tv[6], tv[7]};
+    load_v(b + stride);
+    for (int a = 0; a < cp.nplans; ++a) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int e = lane + 32 * r, pp = e & 15, j = e >> 4;
+        Ure[j * ld + pp] = cur[r].x;
+        Uim[j * ld + pp] = cur[r].y;
+      }
+      __syncwarp();
+      coef_frame_mma(lane, Ure, Uim, lam + (size_t)b * M, M, D, cp.alg[a], cp.coef[a], b, cp.cnt[a], cp.info[a]);
+    }
   }
 }
 
@@ -400,8 +401,6 @@ __global__ void __launch_bounds__(kCoefBigWarps * 32) coef_big_kernel(const doub
 constexpr int kCtaWarps = 8;
 constexpr int kScanNA = 8;        // 8-angle tiles per block (a lane owns 2*NA consecutive angles)
 constexpr int kScanMinBlocks = 2; // __launch_bounds__ min blocks per SM
-constexpr long long kInfBits = 0x7FF0000000000000LL;        // bits of +inf
-constexpr long long kFloorBits = 0x01A56E1FC2F8F359LL;      // bits of 1e-300 (kFloor, Q12)
 
 // Shape by k-steps S (M <= 64 -> S <= 32): 8 tiles of 8 angles per block; S <= 8 (M <= 16) keeps
 // the A fragments of a group in registers with a one-group prefetch and uses two blocks per column
@@ -655,19 +654,21 @@ cudaError_t launch_scan_cta(const doa_plan_s* p, int64_t B, float* P, cudaStream
 }
 
 // ---------------------------------------------------------------------------------------------
-// S7: one warp per frame.  Rank every stored candidate by (f ascending, index ascending) and
-// scatter the first D (PeakSelection; Q11).
-__global__ void __launch_bounds__(128) select_kernel(int64_t B, int D, int cap, const int32_t* __restrict__ cnt,
-                                                    const int32_t* __restrict__ cidx, const double* __restrict__ cf,
-                                                    int32_t* __restrict__ idx, float* __restrict__ val,
-                                                    int32_t* __restrict__ npk, int32_t* __restrict__ info) {
+// S7: one warp per (plan, frame).  Rank every stored candidate by (f ascending, index ascending)
+// and scatter the first D (PeakSelection; Q11).  One launch serves up to kMaxCoefPlans
+// plans (blockIdx.y = plan).
+__global__ void __launch_bounds__(128) select_kernel(int64_t B, int D, SelectPlans sp) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t b = (int64_t)blockIdx.x * 4 + warp;
+  const int a = blockIdx.y;
   if (b >= B) return;
-  const int nraw = cnt[b];
+  const int cap = sp.cap[a];
+  const int nraw = sp.cnt[a][b];
   const int n = nraw < cap ? nraw : cap;
-  const int32_t* ci = cidx + (size_t)b * cap;
-  const double* cfv = cf + (size_t)b * cap;
+  const int32_t* ci = sp.cidx[a] + (size_t)b * cap;
+  const double* cfv = sp.cf[a] + (size_t)b * cap;
+  int32_t* idx = sp.idx[a];
+  float* val = sp.val[a];
   for (int c = lane; c < n; c += 32) {
     const double fc = cfv[c];
     const int ic = ci[c];
@@ -686,41 +687,73 @@ __global__ void __launch_bounds__(128) select_kernel(int64_t B, int D, int cap, 
     val[(size_t)b * D + k] = 0.0f;
   }
   if (lane == 0) {
-    npk[b] = n < D ? n : D;
+    sp.npk[a][b] = n < D ? n : D;
     int fl = 0;
     if (nraw > cap) fl |= DOA_INFO_CAND_OVERFLOW;
     if (n < D) fl |= DOA_INFO_UNDERDETERMINED;
-    if (fl) info[b] |= fl;
+    if (fl) sp.info[a][b] |= fl;
   }
 }
 
 }  // namespace
 
+cudaError_t launch_coef_multi(const doa_plan_s* const* plans, int nplans, const double* lam, const double* V,
+                              int64_t B, int32_t* const* info, cudaStream_t s) {
+  const int M = plans[0]->M;
+  if (M <= 16) {
+    CoefPlans cp = {};
+    for (int a0 = 0; a0 < nplans; a0 += kMaxCoefPlans) {
+      cp.nplans = nplans - a0 < kMaxCoefPlans ? nplans - a0 : kMaxCoefPlans;
+      for (int a = 0; a < cp.nplans; ++a) {
+        const doa_plan_s* q = plans[a0 + a];
+        cp.alg[a] = q->alg; cp.coef[a] = q->coef; cp.cnt[a] = q->cnt; cp.info[a] = info[a0 + a];
+      }
+      const size_t smem = (size_t)kCoefMmaWarps * 2 * kCoefMmaPlane * sizeof(double);
+      const int occ = kernel_occupancy(coef_mma_kernel, kCoefMmaWarps * 32, smem);
+      int64_t nb = (B + kCoefMmaWarps - 1) / kCoefMmaWarps;
+      const int64_t slots = (int64_t)sm_count() * occ * kCoefWaves;
+      if (nb > slots) nb = slots;
+      count_launch();
+      coef_mma_kernel<<<(unsigned)nb, kCoefMmaWarps * 32, smem, s>>>(lam, reinterpret_cast<const double2*>(V), B, M,
+                                                                     plans[0]->D, cp);
+      const cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  for (int a = 0; a < nplans; ++a) {
+    const doa_plan_s* p = plans[a];
+    auto go = [&](auto kern, size_t smem) {
+      kernel_occupancy(kern, kCoefBigWarps * 32, smem);               // sets the smem attribute
+      count_launch();
+      kern<<<(unsigned)B, kCoefBigWarps * 32, smem, s>>>(lam, reinterpret_cast<const double2*>(V), B, M, p->D, p->alg,
+                                                         p->coef, p->cnt, info[a]);
+    };
+    if (M <= 32) go(coef_big_kernel<32>, CoefBig<32>::SMEM);
+    else go(coef_big_kernel<64>, CoefBig<64>::SMEM);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t launch_coef(const doa_plan_s* p, const double* lam, const double* V, int64_t B, int32_t* info,
                         cudaStream_t s) {
-  const int M = p->M;
-  count_launch();
-  if (M <= 16) {
-    const size_t smem = (size_t)kCoefMmaWarps * 2 * kCoefMmaPlane * sizeof(double);
-    const int occ = kernel_occupancy(coef_mma_kernel, kCoefMmaWarps * 32, smem);
-    int64_t nb = (B + kCoefMmaWarps - 1) / kCoefMmaWarps;
-    const int64_t slots = (int64_t)sm_count() * occ * kCoefWaves;
-    if (nb > slots) nb = slots;
-    coef_mma_kernel<<<(unsigned)nb, kCoefMmaWarps * 32, smem, s>>>(
-        lam, reinterpret_cast<const double2*>(V), B, M, p->D, p->alg, p->coef, p->cnt, info);
-    return cudaGetLastError();
-  }
-  auto go = [&](auto kern, size_t smem) {
-    kernel_occupancy(kern, kCoefBigWarps * 32, smem);                 // sets the smem attribute
-    kern<<<(unsigned)B, kCoefBigWarps * 32, smem, s>>>(lam, reinterpret_cast<const double2*>(V), B, M, p->D, p->alg,
-                                                       p->coef, p->cnt, info);
-  };
-  if (M <= 32) go(coef_big_kernel<32>, CoefBig<32>::SMEM);
-  else go(coef_big_kernel<64>, CoefBig<64>::SMEM);
-  return cudaGetLastError();
+  return launch_coef_multi(&p, 1, lam, V, B, &info, s);
+}
+
+bool direct_compatible(const doa_plan_s* a, const doa_plan_s* b) {
+  return a->geom == 0 && b->geom == 0 && a->M == b->M && a->dl == b->dl && a->theta0 == b->theta0 &&
+         a->dtheta == b->dtheta && a->L == b->L && a->mirror == b->mirror && a->cap == b->cap;
 }
 
 cudaError_t launch_scan(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
+  if (B <= kDirectMaxB) {                                 // small batch: direct scan (scan_direct.cu)
+    DirectScanArgs a = {};
+    a.nplans = 1;
+    a.coef[0] = p->coef; a.cnt[0] = p->cnt; a.cidx[0] = p->cand_idx; a.cf[0] = p->cand_f; a.P[0] = P;
+    return launch_scan_direct(a, p, B, s);
+  }
   switch (ksteps(p->M)) {
 #define DOA_SCAN_CASE(k) \
   case k: return p->mirror ? launch_scan_cta<k, true>(p, B, P, s) : launch_scan_cta<k, false>(p, B, P, s);
@@ -735,12 +768,20 @@ cudaError_t launch_scan(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s
   }
 }
 
+cudaError_t launch_select_multi(const SelectPlans& sp, int D, int64_t B, cudaStream_t s) {
+  if (B <= 0 || sp.nplans <= 0) return cudaSuccess;
+  count_launch();
+  select_kernel<<<dim3((unsigned)((B + 3) / 4), (unsigned)sp.nplans), 128, 0, s>>>(B, D, sp);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_select(const doa_plan_s* p, int64_t B, int32_t* idx, float* val, int32_t* npk, int32_t* info,
                           cudaStream_t s) {
-  count_launch();
-  select_kernel<<<(unsigned)((B + 3) / 4), 128, 0, s>>>(B, p->D, p->cap, p->cnt, p->cand_idx, p->cand_f, idx, val,
-                                                         npk, info);
-  return cudaGetLastError();
+  SelectPlans sp = {};
+  sp.nplans = 1;
+  sp.cnt[0] = p->cnt; sp.cidx[0] = p->cand_idx; sp.cf[0] = p->cand_f; sp.cap[0] = p->cap;
+  sp.idx[0] = idx; sp.val[0] = val; sp.npk[0] = npk; sp.info[0] = info;
+  return launch_select_multi(sp, p->D, B, s);
 }
 
 }  // namespace doa

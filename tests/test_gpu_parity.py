@@ -339,15 +339,25 @@ def test_eig_kernels_bitwise_equal(doa):
 
 
 def test_determinism_and_batch_invariance(doa):
+    """Bitwise determinism; a frame's result does not depend on the batch it is in within one scan
+    regime (B > 16: DMMA contraction); the small-batch direct scan (B <= 16) agrees with it to fp32
+    output rounding and in the peak indices (or a certified tie)."""
     cfg = get_config("c4")
     X = torch.from_numpy(generate(cfg, frames=range(300))).cuda()
     plan = doa.Plan(cfg.M, cfg.D, "mn", cfg.dtheta, max_batch=300)
     a = plan.run(X, want_P=True)
     b = plan.run(X, want_P=True)
-    c = plan.run(X[123:124].contiguous(), want_P=True)
+    c = plan.run(X[100:140].contiguous(), want_P=True)
     for u, v in zip(a, b):
         assert torch.equal(u, v)
-    assert torch.equal(a[0][123:124], c[0]) and torch.equal(a[4][123:124], c[4])
+    assert torch.equal(a[0][100:140], c[0]) and torch.equal(a[4][100:140], c[4])
+    d = plan.run(X[123:124].contiguous(), want_P=True)          # direct scan
+    Pa, Pd = a[4][123].cpu().numpy().astype(np.float64), d[4][0].cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(Pa - Pd) / Pa) <= 1e-6
+    if not torch.equal(a[0][123], d[0][0]):
+        o = _oracle_frame(X[123].cpu().numpy(), "mn", cfg.D, 0.5, cfg.theta0, cfg.dtheta, cfg.L)
+        for g in (a[0][123], d[0][0]):
+            _check_frame(o, g.cpu().numpy(), None, "mn", cfg.M, cfg.D, "frame 123")
 
 
 def test_run_host_matches_device(doa):
