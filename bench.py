@@ -209,7 +209,7 @@ class Workload:
 
     def __init__(self, cfg, is_array, X, B, dev, doa):
         import torch
-        self.cfg, self.B, self.X = cfg, B, X
+        self.cfg, self.B, self.X, self.is_array = cfg, B, X, is_array
         M, D = cfg.M, cfg.D
         if is_array:
             self.plans = [doa.Plan.array(cfg.pos, D, a, cfg.az0, cfg.daz, cfg.naz, cfg.el0, cfg.del_, cfg.nel,
@@ -229,10 +229,12 @@ class Workload:
         self.spec_ev = []
 
     def compute(self, sh, stream=None, record=False):
-        """S1-S7 for the four estimators (doa_run_multi: covariance + eig once, then per plan the
-        coefficients, scan and peak selection) + packing of the peak lists; returns the number of
-        libdoa kernel launches.  record=True additionally times each plan's doa_spectrum (the scan's
-        coefficient + contraction kernels) on the eigenpairs of the step, for the roofline."""
+        """S1-S7 for the four estimators (doa_run_multi: covariance, then the frame kernel —
+        eigendecomposition + the four estimators' coefficients — then one scan launch over the four
+        plans and the peak selection) + packing of the peak lists; returns the number of libdoa
+        kernel launches.  record=True additionally times the dominant kernel on the step's data:
+        the four-plan scan launch (doa_scan_multi on the coefficients doa_run_multi left in the
+        plans; general-array workloads: each plan's doa_spectrum), for the roofline."""
         import torch
         from paper_2007_14135_b200 import binding as bd
         from paper_2007_14135_b200 import dist as pdist
@@ -241,7 +243,15 @@ class Workload:
         hs = [p.h for p in self.plans]
         bd.doa_run_multi(hs, self.X, self.idx, self.val, self.npk, self.info, sh)
         n = bd.doa_last_launch_count()
-        if record:
+        if record and not self.is_array:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            bd.doa_scan_multi(hs, self.B, sh)             # one launch: S4-S6 of all four plans
+            e1.record(stream)
+            self.spec_ev.append((e0, e1))
+            bd.doa_run_multi(hs, self.X, self.idx, self.val, self.npk, self.info, sh)   # restore the outputs
+        elif record:
             bd.doa_covariance(hs[0], self.X, self.R, sh)
             bd.doa_eig(hs[0], self.R, self.lam, self.V, self.info_eig, sh)
             for a, h in enumerate(hs):
@@ -320,12 +330,12 @@ def scan_roofline(wl, is_array, mirrored):
     cfg = wl.cfg
     M, L, B = cfg.M, cfg.L, wl.B
     spec_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in wl.spec_ev)
-    if is_array:                                   # K - 1 = M(M-1) fp64 FMAs per (frame, grid point)
+    if is_array:                                   # K - 1 = M(M-1) fp64 FMAs per (frame, grid point), per plan launch
         scan_flops = 2.0 * M * (M - 1) * L * B
-    elif mirrored:                                 # per mirrored pair: E and O (2(M-1) FMAs), E +- O (2 adds)
-        scan_flops = (2.0 * (M - 1) + 1.0) * L * B
-    else:                                          # 2(M-1) fp64 FMAs per (frame, angle)
-        scan_flops = 4.0 * (M - 1) * L * B
+    elif mirrored:                                 # per mirrored pair: E and O (2(M-1) FMAs), E +- O (2 adds); 4 plans
+        scan_flops = (2.0 * (M - 1) + 1.0) * L * B * len(ALGS)
+    else:                                          # 2(M-1) fp64 FMAs per (frame, angle); 4 plans per launch
+        scan_flops = 4.0 * (M - 1) * L * B * len(ALGS)
     pk = peaks_json()
     fp64_peak = 148 * 64 * 2 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12   # TFLOP/s, guide unit counts
     achieved = scan_flops / (spec_ms / 1e3) / 1e12
@@ -432,15 +442,20 @@ def main():
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath) and cfg.name == "c4" and B == cfg.B:
         with open(tpath) as fh:
-            traffic = json.load(fh).get("scan", {}).get("traffic_bytes")
+            rec = json.load(fh).get("scan", {})
+            traffic = rec.get("traffic_bytes") if rec.get("plans_per_launch") == len(ALGS) else None
     roofline = {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp64_peak, "traffic": traffic,
                 "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one scan launch, ncu --set full "
-                                  "(profiles/traffic.json); algorithmic operand bytes per launch: coef 16.8 MB",
-                "kernel": "doa_spectrum = coef_kernel + scan kernel (FP64 DMMA mma.sync m8n8k4); events "
-                          "bracket both, so the scan's own fraction is higher",
-                "algorithmic_flops_per_point": scan_flops / (L * B), "mirrored_scan": mirrored,
-                "kernel_ms": spec_ms, "share_of_step": spec_ms * len(ALGS) / ms_step,
+                                  "(profiles/traffic.json); algorithmic operand bytes per launch: the four plans' "
+                                  "coefficients, 4 x 16.8 MB",
+                "kernel": ("doa_spectrum per plan (coefficient + array scan kernels)" if is_array else
+                           "scan_cta_kernel (S4-S6, FP64 DMMA mma.sync m8n8k4), one launch over the four "
+                           "estimators' frame groups, timed via doa_scan_multi on the step's coefficients"),
+                "algorithmic_flops_per_point": scan_flops / (L * B * (1 if is_array else len(ALGS))),
+                "mirrored_scan": mirrored,
+                "kernel_ms": spec_ms, "launches_per_step": len(ALGS) if is_array else 1,
+                "share_of_step": spec_ms * (len(ALGS) if is_array else 1) / ms_step,
                 "peak_source": "148 SMs x 64 FP64 lanes x 2 flop x sm_max_mhz (guide unit counts; "
                                "measured DMMA 37.18 / DFMA 34.19 TFLOP/s in profiles/fp64_peaks_r01.txt)"}
     if not is_array:

@@ -172,6 +172,17 @@ doa_status_t doa_run_multi(const doa_plan_t* plans, int32_t nplans, const float*
                            int64_t N, int32_t* idx, float* val, int32_t* npk, int32_t* info,
                            doa_stream_t stream);
 
+/* S4-S6 again, for 1..4 ULA plans that share M, d/lambda and the grid (typically the four
+ * estimators), from the Toeplitz coefficients each plan holds from its most recent doa_spectrum,
+ * doa_run or doa_run_multi call (covering at least B frames): the pseudo-spectrum scan and the
+ * local-maximum candidates (Table 2 Step-5/6) of all the plans in ONE launch, whose CTAs
+ * generate the steering table once for every plan.  The plans' candidate lists are reset and
+ * rebuilt, so doa_peaks on each plan afterwards returns what the producing call returned.  Used to
+ * re-scan and to time the scan stage on its own (bench.py's roofline).  Errors: general-array
+ * plans -> DOA_ERR_UNSUPPORTED; plans that differ in the grid, nplans > 4, or B above the frames
+ * the plans hold coefficients for -> DOA_ERR_INVALID_ARG (nothing enqueued). */
+doa_status_t doa_scan_multi(const doa_plan_t* plans, int32_t nplans, int64_t B, doa_stream_t stream);
+
 /* End-to-end variant of doa_run with HOST buffers, for nplans >= 1 plans that share M and D
  * (typically the four estimators): X_host complex64 [B][N][M] is copied host->device in chunks
  * on a second stream into device staging owned by plans[0], overlapping each chunk's copy with

@@ -5,8 +5,10 @@ ctypes binding (binding.py) plus the frame-sharding driver for several GPUs (dis
 """
 from .binding import (ALG, INFO_CAND_OVERFLOW, INFO_DEGENERATE, INFO_NOCONV, INFO_UNDERDETERMINED, DoaError,
                       Plan, doa_covariance, doa_eig, doa_generate, doa_last_launch_count, doa_peaks, doa_plan_create,
-                      doa_plan_destroy, doa_run, doa_run_host, doa_run_multi, doa_spectrum, lib, run_multi)
+                      doa_plan_destroy, doa_run, doa_run_host, doa_run_multi, doa_scan_multi, doa_spectrum, lib,
+                      run_multi)
 
 __all__ = ["ALG", "INFO_CAND_OVERFLOW", "INFO_DEGENERATE", "INFO_NOCONV", "INFO_UNDERDETERMINED", "DoaError",
            "Plan", "doa_covariance", "doa_eig", "doa_generate", "doa_last_launch_count", "doa_peaks", "doa_plan_create",
-           "doa_plan_destroy", "doa_run", "doa_run_host", "doa_run_multi", "doa_spectrum", "lib", "run_multi"]
+           "doa_plan_destroy", "doa_run", "doa_run_host", "doa_run_multi", "doa_scan_multi", "doa_spectrum", "lib",
+           "run_multi"]

@@ -21,7 +21,8 @@ STATUS = {0: "DOA_OK", 1: "DOA_ERR_INVALID_ARG", 2: "DOA_ERR_UNSUPPORTED", 3: "D
 
 EXPORTS = ("doa_generate", "doa_plan_create", "doa_plan_create_array", "doa_plan_destroy", "doa_plan_capacity",
            "doa_plan_info", "doa_covariance", "doa_eig",
-           "doa_spectrum", "doa_peaks", "doa_run", "doa_run_multi", "doa_run_host", "doa_last_launch_count",
+           "doa_spectrum", "doa_peaks", "doa_run", "doa_run_multi", "doa_scan_multi", "doa_run_host",
+           "doa_last_launch_count",
            "doa_status_string", "doa_last_error", "doa_version")
 
 
@@ -56,6 +57,7 @@ def _load():
     L.doa_run.argtypes = [vp, fp, i64, i64, i32p, fp, i32p, fp, i32p, vp]
     L.doa_run_host.argtypes = [C.POINTER(C.c_void_p), i32, fp, i64, i64, i32p, fp, i32p, i32p, vp]
     L.doa_run_multi.argtypes = [C.POINTER(C.c_void_p), i32, fp, i64, i64, i32p, fp, i32p, i32p, vp]
+    L.doa_scan_multi.argtypes = [C.POINTER(C.c_void_p), i32, i64, vp]
     L.doa_generate.argtypes = [i32, d, i32, dp, i32, d, C.c_uint64, i64, i64, i64, fp, vp]
     L.doa_last_launch_count.restype = i32
     L.doa_status_string.argtypes = [C.c_int]
@@ -264,6 +266,16 @@ def doa_run_multi(plans, X, idx, val, npk, info, stream=None):
     arr = (C.c_void_p * n)(*[_hval(p) for p in plans])
     _check(lib.doa_run_multi(arr, n, _ptr(_f32(X)), B, N, _ptr(idx), _ptr(val), _ptr(npk), _ptr(info),
                              _stream(stream)))
+
+
+def doa_scan_multi(plans, B, stream=None):
+    """S4-S6 again for 1..4 grid-sharing ULA plans from the coefficients they hold (include/doa.h);
+    the candidate lists are rebuilt for a following doa_peaks.  One launch."""
+    if not isinstance(plans, (list, tuple)):
+        plans = [plans]
+    n = len(plans)
+    arr = (C.c_void_p * n)(*[_hval(p) for p in plans])
+    _check(lib.doa_scan_multi(arr, n, int(B), _stream(stream)))
 
 
 def run_multi(plans, X, stream=None):

@@ -81,47 +81,62 @@ cudaError_t spectrum_stage(const doa_plan_s* p, const double* lam, const double*
   return doa::launch_scan(p, B, P, s);
 }
 
-// S1-S7 for nplans plans sharing M and D on device buffers (doa_run_multi, and doa_run_host per
-// chunk): covariance and eigendecomposition once (plans[0]'s scratch), then per plan the
-// coefficients, the scan — for small batches the direct scan, one launch per group of up to four
-// plans that share the grid — and the peak selection.  Plan a's outputs live at idx + a*ldo*D,
-// val + a*ldo*D, npk + a*ldo, info + a*ldo.
+// S4-S6 for the ULA plans among plans[0..nplans): consecutive direct-compatible plans share one scan
+// launch (up to kMaxCoefPlans); the coefficients must be in place and the counters zeroed.
+// P (nullable) is used only when nplans == 1.
+cudaError_t scan_stage(doa_plan_s* const* plans, int nplans, int64_t B, float* P, cudaStream_t st) {
+  cudaError_t e = cudaSuccess;
+  for (int a = 0; a < nplans && e == cudaSuccess;) {
+    if (plans[a]->geom == 1) { ++a; continue; }
+    const doa_plan_s* grp[doa::kMaxCoefPlans] = {};
+    int n = 0;
+    while (a < nplans && n < doa::kMaxCoefPlans && plans[a]->geom == 0 &&
+           (n == 0 || doa::direct_compatible(plans[a], grp[0])))
+      grp[n++] = plans[a++];
+    e = doa::launch_scan_plans(grp, n, B, nplans == 1 ? P : nullptr, st);
+  }
+  return e;
+}
+
+// S1-S7 for nplans plans sharing M and D on device buffers (doa_run_multi, doa_run, and doa_run_host
+// per chunk): the covariance once (plans[0]'s scratch); for M <= 16 and up to kMaxCoefPlans ULA
+// plans the frame kernel (eigendecomposition + every plan's coefficients in one launch, V never
+// leaves the SM), otherwise the eigendecomposition once and per plan S3; then the scans (one launch
+// per group of grid-sharing plans) and the peak selection.  Plan a's outputs live at
+// idx + a*ldo*D, val + a*ldo*D, npk + a*ldo, info + a*ldo.
 cudaError_t run_plans(doa_plan_s* const* plans, int nplans, const float* X, int64_t B, int64_t N, int32_t* idx,
                       float* val, int32_t* npk, int32_t* info, int64_t ldo, cudaStream_t st,
-                      cudaEvent_t x_consumed = nullptr) {
+                      cudaEvent_t x_consumed = nullptr, float* P = nullptr) {
   doa_plan_s* p = plans[0];
   const int M = p->M, D = p->D;
   cudaError_t e = doa::launch_covariance(X, B, N, M, p->R, st);
   if (e == cudaSuccess && x_consumed) e = cudaEventRecord(x_consumed, st);   // X no longer needed
-  if (e == cudaSuccess) e = doa::launch_eig(p->R, B, M, p->lam, p->V, info, st);
-  for (int a = 1; a < nplans && e == cudaSuccess; ++a)        // every plan starts from the eig flags
-    e = cudaMemcpyAsync(info + (size_t)a * ldo, info, (size_t)B * sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
-  {                                                   // S3: one coefficient launch for the ULA plans
+  bool fused = M <= 16 && nplans <= doa::kMaxCoefPlans;
+  for (int a = 0; a < nplans; ++a) fused &= plans[a]->geom == 0;
+  if (fused) {
+    doa::CoefPlans cp = {};
+    cp.nplans = nplans;
+    for (int a = 0; a < nplans; ++a) {
+      cp.alg[a] = plans[a]->alg; cp.coef[a] = plans[a]->coef; cp.cnt[a] = plans[a]->cnt;
+      cp.info[a] = info + (size_t)a * ldo;
+    }
+    if (e == cudaSuccess) e = doa::launch_eig16_coef(p->R, B, M, D, nullptr, nullptr, cp, st);
+  } else {
+    if (e == cudaSuccess) e = doa::launch_eig(p->R, B, M, p->lam, p->V, info, st);
+    for (int a = 1; a < nplans && e == cudaSuccess; ++a)        // every plan starts from the eig flags
+      e = cudaMemcpyAsync(info + (size_t)a * ldo, info, (size_t)B * sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
     const doa_plan_s* ula[64];
     int32_t* ula_info[64];
     int nu = 0;
     for (int a = 0; a < nplans && e == cudaSuccess; ++a) {
       doa_plan_s* q = plans[a];
-      if (q->geom == 1) e = doa::launch_array_spectrum(q, p->lam, p->V, B, nullptr, info + (size_t)a * ldo, st);
+      if (q->geom == 1) e = doa::launch_array_spectrum(q, p->lam, p->V, B, nplans == 1 ? P : nullptr, info + (size_t)a * ldo, st);
       else if (nu < 64) { ula[nu] = q; ula_info[nu++] = info + (size_t)a * ldo; }
       else e = doa::launch_coef(q, p->lam, p->V, B, info + (size_t)a * ldo, st);
     }
     if (e == cudaSuccess && nu) e = doa::launch_coef_multi(ula, nu, p->lam, p->V, B, ula_info, st);
   }
-  for (int a = 0; a < nplans && e == cudaSuccess;) {
-    doa_plan_s* q = plans[a];
-    if (q->geom == 1) { ++a; continue; }
-    if (B > doa::kDirectMaxB) { e = doa::launch_scan(q, B, nullptr, st); ++a; continue; }
-    doa::DirectScanArgs da = {};
-    int n = 0;
-    while (a < nplans && n < doa::kMaxDirectPlans && doa::direct_compatible(q, plans[a])) {
-      doa_plan_s* r = plans[a++];
-      da.coef[n] = r->coef; da.cnt[n] = r->cnt; da.cidx[n] = r->cand_idx; da.cf[n] = r->cand_f; da.P[n] = nullptr;
-      ++n;
-    }
-    da.nplans = n;
-    e = doa::launch_scan_direct(da, q, B, st);
-  }
+  if (e == cudaSuccess) e = scan_stage(plans, nplans, B, P, st);
   for (int a0 = 0; a0 < nplans && e == cudaSuccess; a0 += 4) {     // S7: one launch per 4 plans
     doa::SelectPlans sp = {};
     sp.nplans = nplans - a0 < 4 ? nplans - a0 : 4;
@@ -132,6 +147,7 @@ cudaError_t run_plans(doa_plan_s* const* plans, int nplans, const float* X, int6
       sp.idx[k] = idx + a * ldo * D; sp.val[k] = val + a * ldo * D; sp.npk[k] = npk + a * ldo;
       sp.info[k] = info + a * ldo;
       q->last_B = B;
+      q->coef_B = q->geom == 0 ? B : 0;
     }
     e = doa::launch_select_multi(sp, D, B, st);
   }
@@ -374,6 +390,7 @@ doa_status_t doa_spectrum(doa_plan_t p, const double* lambda, const double* V, i
   if (P && !aligned(P, 4)) return fail(DOA_ERR_INVALID_ARG, "doa_spectrum: P is not 4-byte aligned");
   DOA_TRY(spectrum_stage(p, lambda, V, B, P, info, (cudaStream_t)s), "doa_spectrum");
   p->last_B = B;
+  p->coef_B = p->geom == 0 ? B : 0;
   return DOA_OK;
 }
 
@@ -407,13 +424,8 @@ doa_status_t doa_run(doa_plan_t p, const float* X, int64_t B, int64_t N, int32_t
   DOA_CHECK_PTR(npk, 4);
   DOA_CHECK_PTR(info, 4);
   if (P && !aligned(P, 4)) return fail(DOA_ERR_INVALID_ARG, "doa_run: P is not 4-byte aligned");
-  cudaStream_t st = (cudaStream_t)s;
   DOA_TRY(ensure_run_scratch(p), "doa_run: scratch allocation");
-  DOA_TRY(doa::launch_covariance(X, B, N, p->M, p->R, st), "doa_run/covariance");
-  DOA_TRY(doa::launch_eig(p->R, B, p->M, p->lam, p->V, info, st), "doa_run/eig");
-  DOA_TRY(spectrum_stage(p, p->lam, p->V, B, P, info, st), "doa_run/spectrum");
-  DOA_TRY(doa::launch_select(p, B, idx, val, npk, info, st), "doa_run/select");
-  p->last_B = B;
+  DOA_TRY(run_plans(&p, 1, X, B, N, idx, val, npk, info, B, (cudaStream_t)s, nullptr, P), "doa_run");
   return DOA_OK;
 }
 
@@ -431,6 +443,32 @@ doa_status_t doa_run_multi(const doa_plan_t* plans, int32_t nplans, const float*
   DOA_CHECK_PTR(info, 4);
   DOA_TRY(ensure_run_scratch(plans[0]), "doa_run_multi: scratch allocation");
   DOA_TRY(run_plans(plans, nplans, X, B, N, idx, val, npk, info, B, (cudaStream_t)s), "doa_run_multi");
+  return DOA_OK;
+}
+
+doa_status_t doa_scan_multi(const doa_plan_t* plans, int32_t nplans, int64_t B, doa_stream_t s) {
+  g_launches = 0;
+  const doa_status_t st = check_plan_set("doa_scan_multi", plans, nplans, B);
+  if (st != DOA_OK) return st;
+  if (nplans > doa::kMaxCoefPlans)
+    return fail(DOA_ERR_INVALID_ARG, "doa_scan_multi: nplans=%d > %d", nplans, doa::kMaxCoefPlans);
+  for (int a = 0; a < nplans; ++a) {
+    if (plans[a]->geom != 0) return fail(DOA_ERR_UNSUPPORTED, "doa_scan_multi: plans[%d] is a general-array plan", a);
+    if (a > 0 && !doa::direct_compatible(plans[a], plans[0]))
+      return fail(DOA_ERR_INVALID_ARG, "doa_scan_multi: plans[%d] does not share the grid of plans[0]", a);
+    if (B > plans[a]->coef_B)
+      return fail(DOA_ERR_INVALID_ARG, "doa_scan_multi: plans[%d] holds coefficients for %lld frames, B=%lld", a,
+                  (long long)plans[a]->coef_B, (long long)B);
+  }
+  if (B == 0) return DOA_OK;
+  cudaStream_t st2 = (cudaStream_t)s;
+  const doa_plan_s* grp[doa::kMaxCoefPlans] = {};
+  for (int a = 0; a < nplans; ++a) {
+    grp[a] = plans[a];
+    DOA_TRY(cudaMemsetAsync(plans[a]->cnt, 0, (size_t)B * sizeof(int32_t), st2), "doa_scan_multi: counters");
+  }
+  DOA_TRY(doa::launch_scan_plans(grp, nplans, B, nullptr, st2), "doa_scan_multi");
+  for (int a = 0; a < nplans; ++a) plans[a]->last_B = B;
   return DOA_OK;
 }
 
@@ -499,7 +537,7 @@ doa_status_t doa_run_host(const doa_plan_t* plans, int32_t nplans, const float* 
                       d_info + b0, B, st, p->ev_used[k]), "doa_run_host/run");
     launches += g_launches;
   }
-  for (int a = 0; a < nplans; ++a) plans[a]->last_B = 0;
+  for (int a = 0; a < nplans; ++a) plans[a]->last_B = plans[a]->coef_B = 0;
   const size_t nBD = (size_t)nplans * B * D, nB = (size_t)nplans * B;
   DOA_TRY(cudaMemcpyAsync(idx_host, d_idx, nBD * sizeof(int32_t), cudaMemcpyDeviceToHost, st), "D2H");
   DOA_TRY(cudaMemcpyAsync(val_host, d_val, nBD * sizeof(float), cudaMemcpyDeviceToHost, st), "D2H");

@@ -79,6 +79,7 @@ struct doa_plan_s {
   double* dpos;                   // [M(M-1)/2][3] device
   double* fbuf;                   // [max_batch][L] floored f of the last doa_spectrum (device)
   int64_t last_B;                 // B of the last doa_spectrum (consumed by doa_peaks)
+  int64_t coef_B;                 // frames whose S3 coefficients the plan holds (doa_scan_multi)
   // workspace (device)
   int32_t* cnt;                   // [max_batch]           candidate counters
   int32_t* cand_idx;              // [max_batch][cap]
@@ -113,9 +114,23 @@ struct CoefPlans {
   int32_t* info[kMaxCoefPlans];
   int nplans;
 };
+// The frame kernel for M <= 16 (csrc/eig16.cu): S2 + S3 for up to kMaxCoefPlans ULA plans in one
+// launch; lam / V nullable (not written); each plan's info[b] is overwritten (NOCONV | DEGENERATE).
+cudaError_t launch_eig16_coef(const double* R, int64_t B, int M, int D, double* lam, double* V, const CoefPlans& cp,
+                              cudaStream_t s);
 cudaError_t launch_coef_multi(const doa_plan_s* const* plans, int nplans, const double* lam, const double* V,
                               int64_t B, int32_t* const* info, cudaStream_t s);
 cudaError_t launch_scan(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s);
+// S4-S6 for 1..kMaxCoefPlans direct_compatible ULA plans (coefficients in place, counters zeroed) in
+// one launch; P (nplans == 1 only) nullable
+struct ScanPlans {
+  const double* coef[kMaxCoefPlans];
+  int32_t* cnt[kMaxCoefPlans];
+  int32_t* cidx[kMaxCoefPlans];
+  double* cf[kMaxCoefPlans];
+  int nplans;
+};
+cudaError_t launch_scan_plans(const doa_plan_s* const* plans, int nplans, int64_t B, float* P, cudaStream_t s);
 cudaError_t launch_select(const doa_plan_s* p, int64_t B, int32_t* idx, float* val, int32_t* npk, int32_t* info,
                           cudaStream_t s);
 // S7 for up to kMaxCoefPlans plans sharing D in one launch

@@ -74,6 +74,135 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {   // conj(a) * 
   return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
 }
 
+// ---------------------------------------------------------------------------------------------
+// S3 in the eigensolver's epilogue (the "frame kernel"): Table 3's Step-3/4
+// for up to kMaxCoefPlans estimators straight from the converged eigenpairs, reduced to
+// the Toeplitz sums c_k = sum_p C[p][p+k] of DESIGN.md §5, so V never leaves the SM.  With
+// g_{k,j} = sum_{p < M-k} V[p][j] conj(V[p+k][j]) (column j = eigenvector of the j-th smallest
+// eigenvalue, Q2):
+//   PHD   c_k = g_{k,0}                                   (C = e_min e_min^H, Q4)
+//   MUSIC c_k = sum_{j<K} g_{k,j}                          (C = E_n E_n^H, K = M - D)
+//   EV    c_k = sum_{j<K} w_j g_{k,j}, w_j = 1/lambda_j    (Q1; clamped at 100 eps lambda_max, G1)
+//   MN    c_k = sum_{p < M-k} w_p conj(w_{p+k}),  w = P_n e1 / (e1^H P_n e1),
+//         (P_n e1)_p = sum_{j<K} V[p][j] conj(V[0][j])     (Q5; e1^H P_n e1 <= 100 eps: unnormalised, G1)
+// Executed by a 16-lane group (hl = lane within it); every sum runs in a fixed ascending order, so
+// eig16h and eig16s (same eigenpairs, same routine) give bitwise identical coefficients.
+//   Vs   [N][N+1] eigenvectors in rank order, Vs[p (N+1) + j] = V[p][j] (written by the caller)
+//   lam  [N] ascending eigenvalues;  Gs [N][N+1], Ws [N], Es [N]: scratch
+// Outputs per plan a: coefficients in the scan's A-fragment layout (coef_index), cnt[b] = 0 and
+// info[b] = eigflag | DEGENERATE (overwritten).  `live`: this group holds a real frame b < B.
+template <int N>
+__device__ __forceinline__ void frame_coef(int hl, unsigned gmask, const double2* Vs, const double* lam, double2* Gs,
+                                           double2* Ws, double* Es, int M, int D, const CoefPlans& cp, int64_t b,
+                                           bool live, int eigflag) {
+  constexpr int LDV = N + 1;
+  const int K = M - D;
+  bool need_ev = false, need_mn = false;
+#pragma unroll
+  for (int a = 0; a < kMaxCoefPlans; ++a)
+    if (a < cp.nplans) { need_ev |= cp.alg[a] == DOA_ALG_EV; need_mn |= cp.alg[a] == DOA_ALG_MN; }
+  // (a) lane j: g_{k,j} for every lag k from column j (zero beyond M)
+  {
+    const int j = hl;
+    double2 col[N];
+#pragma unroll
+    for (int p = 0; p < N; ++p) col[p] = (j < M && p < M) ? Vs[p * LDV + j] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double gr = 0.0, gi = 0.0;
+#pragma unroll
+      for (int p = 0; p + k < N; ++p) {                 // V[p][j] conj(V[p+k][j]), ascending p
+        gr = fma(col[p].x, col[p + k].x, gr);
+        gr = fma(col[p].y, col[p + k].y, gr);
+        gi = fma(col[p].y, col[p + k].x, gi);
+        gi = fma(-col[p].x, col[p + k].y, gi);
+      }
+      if (j < N) Gs[k * LDV + j] = make_double2(gr, gi);
+    }
+  }
+  int flag_ev = 0, flag_mn = 0;
+  if (need_ev) {                                        // EV weights, lane-parallel (G1 clamp)
+    const double lfloor = 100.0 * DBL_EPSILON * fmax(lam[M - 1], 0.0);
+    const double lj = hl < K ? lam[hl] : 1.0;
+    const bool deg = hl < K && lj <= lfloor;
+    if (__ballot_sync(0xffffffffu, deg) & gmask) flag_ev = DOA_INFO_DEGENERATE;
+    Es[hl] = hl < K ? (deg ? (lfloor > 0.0 ? 1.0 / lfloor : 1.0) : 1.0 / lj) : 0.0;
+  }
+  if (need_mn) {                                        // w_p on lane p, p0 on every lane (same order)
+    const int p = hl;
+    double wr = 0.0, wi = 0.0, p0 = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      if (j < K) {
+        const double2 v0 = Vs[j], vp = p < M ? Vs[p * LDV + j] : make_double2(0.0, 0.0);
+        wr = fma(vp.x, v0.x, wr);                       // V[p][j] conj(V[0][j])
+        wr = fma(vp.y, v0.y, wr);
+        wi = fma(vp.y, v0.x, wi);
+        wi = fma(-vp.x, v0.y, wi);
+        p0 = fma(v0.x, v0.x, p0);
+        p0 = fma(v0.y, v0.y, p0);
+      }
+    }
+    const bool degen = !(p0 > 100.0 * DBL_EPSILON);
+    if (degen) flag_mn = DOA_INFO_DEGENERATE;
+    const double lp = degen ? 1.0 : 1.0 / p0;
+    Ws[p] = degen ? make_double2(wr, wi) : make_double2(wr * lp, wi * lp);   // zero for p >= M
+  }
+  __syncwarp();
+  // (b) lane k: combine over j (ascending) and write every plan's coefficients
+  const int k = hl;
+  double2 phd = make_double2(0.0, 0.0), mus = phd, ev = phd, mn = phd;
+  if (k < M) {
+    phd = Gs[k * LDV];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      if (j < K) {
+        const double2 g = Gs[k * LDV + j];
+        mus.x += g.x;
+        mus.y += g.y;
+        if (need_ev) {
+          const double w = Es[j];
+          ev.x = fma(w, g.x, ev.x);
+          ev.y = fma(w, g.y, ev.y);
+        }
+      }
+    }
+    if (need_mn) {
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+        if (p + k < M) {                                // w_p conj(w_{p+k}), ascending p
+          const double2 x = Ws[p], y = Ws[p + k];
+          mn.x = fma(x.x, y.x, mn.x);
+          mn.x = fma(x.y, y.y, mn.x);
+          mn.y = fma(x.y, y.x, mn.y);
+          mn.y = fma(-x.x, y.y, mn.y);
+        }
+      }
+    }
+  }
+  const int S = ksteps(M), JE = 4 * ksteps_even(M);
+#pragma unroll
+  for (int a = 0; a < kMaxCoefPlans; ++a) {
+    if (a >= cp.nplans || !live) continue;
+    const int alg = cp.alg[a];
+    double* coef = cp.coef[a];
+    const double2 c = alg == DOA_ALG_PHD ? phd : (alg == DOA_ALG_MUSIC ? mus : (alg == DOA_ALG_EV ? ev : mn));
+    if (k < M) {
+      if (k == 0) coef[coef_index(b, 0, S)] = c.x;
+      else {
+        coef[coef_index(b, coef_cos(k), S)] = 2.0 * c.x;
+        coef[coef_index(b, coef_sin(M, k), S)] = 2.0 * c.y;
+      }
+    }
+    for (int jj = hl; jj < 4 * S; jj += 16)                                          // K padding
+      if ((jj >= M && jj < JE) || jj >= JE + M - 1) coef[coef_index(b, jj, S)] = 0.0;
+    if (hl == 0) {
+      cp.cnt[a][b] = 0;
+      cp.info[a][b] = eigflag | (alg == DOA_ALG_EV ? flag_ev : 0) | (alg == DOA_ALG_MN ? flag_mn : 0);
+    }
+  }
+}
+
 // eig16h (batches): two matrices per warp, one per 16-lane half.  Phase 1 of both matrices runs
 // in the same instructions (lanes 0-7 and 16-23); each lane of a half owns one full row of V (16
 // complex) and two of the 28 off-diagonal blocks.  A converged matrix keeps running with identity
@@ -107,15 +236,20 @@ __host__ __device__ constexpr int cat_next_c(int s, int n) {
 template <int N>
 __device__ __forceinline__ int cat_nextT(int s) { return cat_next_c(s, N); }
 
-template <int N>
+// FUSE: the frame kernel — S3 for the plans in `cp` runs in the epilogue (frame_coef); lam_out /
+// V_out / info may then be NULL (not written).
+template <int N, bool FUSE>
 __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(const double2* __restrict__ R,
                                                                              int64_t B, int M,
                                                                              double* __restrict__ lam_out,
                                                                              double2* __restrict__ V_out,
-                                                                             int32_t* __restrict__ info) {
+                                                                             int32_t* __restrict__ info,
+                                                                             int D, CoefPlans cp) {
   __shared__ double2 As[kHWarps][2][2][N * HLd<N>::LD];          // [warp][half][buffer]
   __shared__ Prm prm[kHWarps][2][N / 2];
   __shared__ int rank_s[kHWarps][2][N];
+  __shared__ double lam_s[FUSE ? kHWarps : 1][2][16], es_s[FUSE ? kHWarps : 1][2][16];
+  __shared__ double2 ws_s[FUSE ? kHWarps : 1][2][16];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int hm = lane >> 4, hl = lane & 15;
   const int64_t b = ((int64_t)blockIdx.x * kHWarps + warp) * 2 + hm;
@@ -280,16 +414,30 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
       rk += (lj < li) || (lj == li && j < hl);
     }
     rank_s[warp][hm][hl] = rk;
-    if (valid) lam_out[(size_t)b * M + rk] = li;
+    if (valid && lam_out) lam_out[(size_t)b * M + rk] = li;
+    if (FUSE) lam_s[FUSE ? warp : 0][hm][rk] = li;
   }
   __syncwarp();
-  if (valid && hl < M) {
+  if (valid && hl < M && V_out) {
     double2* Vrow = V_out + (size_t)b * M * M + (size_t)hl * M;
 #pragma unroll
     for (int k = 0; k < N; ++k)
       if (k < M) Vrow[rank_s[warp][hm][k]] = v[k];
   }
-  if (valid && hl == 0) info[b] = flag;
+  if (valid && hl == 0 && info) info[b] = flag;
+  if (FUSE) {
+    // rank-ordered V into the free buffer, then S3 with the A buffer as scratch (its diagonal has
+    // been read by every lane before the __syncwarp above)
+    double2* Vs = As[warp][hm][cur ^ 1];
+    if (hl < M) {
+#pragma unroll
+      for (int k = 0; k < N; ++k)
+        if (k < M) Vs[hl * (N + 1) + rank_s[warp][hm][k]] = v[k];
+    }
+    __syncwarp();
+    frame_coef<N>(hl, hm ? 0xffff0000u : 0x0000ffffu, Vs, lam_s[FUSE ? warp : 0][hm], As[warp][hm][cur],
+                  ws_s[FUSE ? warp : 0][hm], es_s[FUSE ? warp : 0][hm], M, D, cp, b, valid, flag);
+  }
 }
 
 
@@ -338,10 +486,10 @@ __device__ __forceinline__ double2 sel2(bool p, double2 a, double2 b) {
   return make_double2(p ? a.x : b.x, p ? a.y : b.y);
 }
 
-template <int N>
+template <int N, bool FUSE>
 __global__ void __launch_bounds__(64) eig16s_kernel(const double2* __restrict__ R, int64_t B, int M,
                                                     double* __restrict__ lam_out, double2* __restrict__ V_out,
-                                                    int32_t* __restrict__ info) {
+                                                    int32_t* __restrict__ info, int D, CoefPlans cp) {
   constexpr int NP = N / 2, NBLK = NP * (NP - 1) / 2, SPL = N / 2, RPW = 32 / (N / 4) / 2;
   // V: lane l of warp 1 holds row l / (N/8 * ...) -- N = 16: row l/2, slot half l%2; N = 8: row
   // l/2 for l < 16 (lanes 16-31 idle), slot half l%2
@@ -350,6 +498,8 @@ __global__ void __launch_bounds__(64) eig16s_kernel(const double2* __restrict__ 
   __shared__ double Dp[2][N];
   __shared__ int rank_s[N];
   __shared__ int go_s;
+  __shared__ double lam_s[FUSE ? 16 : 1], es_s[FUSE ? 16 : 1];
+  __shared__ double2 ws_s[FUSE ? 16 : 1];
   (void)RPW;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t b = blockIdx.x;
@@ -533,42 +683,69 @@ __global__ void __launch_bounds__(64) eig16s_kernel(const double2* __restrict__ 
       rk += (lj < li) || (lj == li && j < lane);
     }
     rank_s[lane] = rk;
-    lam_out[(size_t)b * M + rk] = li;
+    if (lam_out) lam_out[(size_t)b * M + rk] = li;
+    if (FUSE) lam_s[rk] = li;
   }
   __syncthreads();
   if (warp == 1 && vrow < M) {
-    double2* Vrow = V_out + (size_t)b * M * M + (size_t)vrow * M;
+    if (V_out) {
+      double2* Vrow = V_out + (size_t)b * M * M + (size_t)vrow * M;
 #pragma unroll
-    for (int l = 0; l < SPL; ++l)
-      if (SPL * g + l < M) Vrow[rank_s[SPL * g + l]] = v[l];
+      for (int l = 0; l < SPL; ++l)
+        if (SPL * g + l < M) Vrow[rank_s[SPL * g + l]] = v[l];
+    }
+    if (FUSE) {                                         // rank-ordered V for frame_coef
+#pragma unroll
+      for (int l = 0; l < SPL; ++l)
+        if (SPL * g + l < M) As[0][vrow * (N + 1) + rank_s[SPL * g + l]] = v[l];
+    }
   }
-  if (tid == 0) info[b] = flag;
+  if (tid == 0 && info) info[b] = flag;
+  if (FUSE) {
+    // warp 0 runs S3 on both 16-lane halves (the same frame; only half 0 writes), exactly as one
+    // half of eig16h does, so the coefficients are bitwise the same for any B
+    if (warp == 0) flag = __shfl_sync(0xffffffffu, flag, 0);
+    __syncthreads();
+    if (warp == 0)
+      frame_coef<N>(lane & 15, lane < 16 ? 0x0000ffffu : 0xffff0000u, As[0], lam_s, As[1], ws_s, es_s, M, D, cp, b,
+                    lane < 16, flag);
+  }
 }
 
 }  // namespace
 
-cudaError_t launch_eig16(const double* R, int64_t B, int M, double* lam, double* V, int32_t* info, cudaStream_t s) {
+namespace {
+// Kernel choice for M <= 16: small batches (latency-bound) take the CTA-per-matrix pipelined
+// kernel; it performs the same operations in the same order as eig16h, so the results are bitwise
+// the same (tests/test_gpu_parity.py::test_eig_kernels_bitwise_equal).
+template <bool FUSE>
+cudaError_t launch16(const double* R, int64_t B, int M, double* lam, double* V, int32_t* info, int D,
+                     const CoefPlans& cp, cudaStream_t s) {
   count_launch();
-  // small batches (latency-bound) take the CTA-per-matrix pipelined kernel; it performs the same
-  // operations in the same order as eig16h, so the results are bitwise the same
-  // (tests/test_gpu_parity.py::test_eig_kernels_bitwise_equal)
+  const double2* R2 = reinterpret_cast<const double2*>(R);
+  double2* V2 = reinterpret_cast<double2*>(V);
   if (B < DOA_EIG_HALF_MIN_B) {
-    if (M <= 8)
-      eig16s_kernel<8><<<(unsigned)B, 64, 0, s>>>(reinterpret_cast<const double2*>(R), B, M, lam,
-                                                  reinterpret_cast<double2*>(V), info);
-    else
-      eig16s_kernel<16><<<(unsigned)B, 64, 0, s>>>(reinterpret_cast<const double2*>(R), B, M, lam,
-                                                   reinterpret_cast<double2*>(V), info);
+    if (M <= 8) eig16s_kernel<8, FUSE><<<(unsigned)B, 64, 0, s>>>(R2, B, M, lam, V2, info, D, cp);
+    else eig16s_kernel<16, FUSE><<<(unsigned)B, 64, 0, s>>>(R2, B, M, lam, V2, info, D, cp);
     return cudaGetLastError();
   }
   const unsigned g = (unsigned)((B + 2 * kHWarps - 1) / (2 * kHWarps));
-  if (M <= 8)
-    eig16h_kernel<8><<<g, kHWarps * 32, 0, s>>>(reinterpret_cast<const double2*>(R), B, M, lam,
-                                                 reinterpret_cast<double2*>(V), info);
-  else
-    eig16h_kernel<16><<<g, kHWarps * 32, 0, s>>>(reinterpret_cast<const double2*>(R), B, M, lam,
-                                                  reinterpret_cast<double2*>(V), info);
+  if (M <= 8) eig16h_kernel<8, FUSE><<<g, kHWarps * 32, 0, s>>>(R2, B, M, lam, V2, info, D, cp);
+  else eig16h_kernel<16, FUSE><<<g, kHWarps * 32, 0, s>>>(R2, B, M, lam, V2, info, D, cp);
   return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_eig16(const double* R, int64_t B, int M, double* lam, double* V, int32_t* info, cudaStream_t s) {
+  const CoefPlans none = {};
+  return launch16<false>(R, B, M, lam, V, info, 0, none, s);
+}
+
+// The frame kernel: S2 + S3 in one launch (M <= 16, up to kMaxCoefPlans ULA plans sharing M, D).
+// lam / V may be NULL (not written); every plan's info[b] is overwritten.
+cudaError_t launch_eig16_coef(const double* R, int64_t B, int M, int D, double* lam, double* V, const CoefPlans& cp,
+                              cudaStream_t s) {
+  return launch16<true>(R, B, M, lam, V, nullptr, D, cp, s);
 }
 
 }  // namespace doa

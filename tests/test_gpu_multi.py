@@ -127,3 +127,71 @@ def test_run_multi_rejects_bad_plan_sets(doa):
         doa.run_multi([p16, small], X)                    # B > max_batch of one plan
     for p in (p16, p8, small):
         p.close()
+
+
+# ---------------------------------------------------------------------------------------------
+# The frame kernel (eigendecomposition + S3 of every plan in one launch, M <= 16) and the four-plan
+# scan launch: against the staged path (doa_eig -> doa_spectrum -> doa_peaks, which keeps the
+# separate coefficient kernel), across the eig16s / eig16h boundary, and doa_scan_multi.
+
+@pytest.mark.parametrize("M,D,B", [(16, 4, 300), (8, 2, 40), (12, 3, 2100)])
+def test_frame_kernel_matches_staged_path(doa, M, D, B):
+    cfg = get_config("c4").with_(M=M, D=D, dtheta=0.05)
+    Xn = generate(cfg, frames=range(B))
+    X = torch.from_numpy(Xn).cuda()
+    plans = _plans(doa, cfg, B)
+    idx, val, npk, info = [t.cpu().numpy() for t in doa.run_multi(plans, X)]
+    R = plans[0].covariance(X)
+    lam, V, einfo = plans[0].eig(R)
+    for a, (alg, p) in enumerate(zip(ALGS, plans)):
+        Ps, sinfo = p.spectrum(lam, V, info=einfo.clone(), want_P=True)
+        si, sv, sn, sf = [t.cpu().numpy() for t in p.peaks(B, info=sinfo)]
+        _, _, _, _, Pf = p.run(X, want_P=True)                   # fused path with P (single plan)
+        Ps, Pf = Ps.cpu().numpy().astype(np.float64), Pf.cpu().numpy().astype(np.float64)
+        assert np.max(np.abs(Pf - Ps) / Ps) <= 1e-9, alg        # same eigenpairs, S3 rounded differently
+        diff = np.any(idx[a] != si, axis=1) | (npk[a] != sn)
+        assert np.array_equal(info[a][~diff], sf[~diff]), alg
+        for b in np.nonzero(diff)[0]:                            # differences only at certified ties
+            Ro, lo, fo, Cm, oidx = _oracle(Xn[b], alg, cfg)
+            for g in (idx[a, b], si[b]):
+                ok, _, why = certify(g, oidx, fo, delta_bound(alg, M, D, Ro, lo, Cm, fo), D)
+                assert ok, f"{alg} b={b}: {why}"
+    for p in plans:
+        p.close()
+
+
+@pytest.mark.parametrize("M", [8, 16])
+def test_frame_kernel_batch_invariant(doa, M):
+    """B = 2047 runs eig16s (CTA per matrix), B = 2048 eig16h (two matrices per warp): the frame
+    kernel's coefficients, hence every output, are bitwise the same for the common frames."""
+    cfg = get_config("c4").with_(M=M, D=3, dtheta=0.5)
+    X = torch.from_numpy(generate(cfg, frames=range(2048))).cuda()
+    plans = _plans(doa, cfg, 2048)
+    big = doa.run_multi(plans, X)
+    small = doa.run_multi(plans, X[:2047].contiguous())
+    for t_big, t_small in zip(big, small):
+        assert torch.equal(t_big[:, :2047], t_small)
+    for p in plans:
+        p.close()
+
+
+@pytest.mark.parametrize("B", [9, 1000])
+def test_scan_multi_reproduces_run_multi(doa, B):
+    cfg = get_config("c4").with_(dtheta=0.02)
+    X = torch.from_numpy(generate(cfg, frames=range(B))).cuda()
+    plans = _plans(doa, cfg, B)
+    idx, val, npk, info = doa.run_multi(plans, X)
+    doa.doa_scan_multi([p.h for p in plans], B)
+    for a, p in enumerate(plans):
+        i2, v2, n2, f2 = p.peaks(B, info=info[a].clone())
+        assert torch.equal(i2, idx[a]) and torch.equal(v2, val[a]) and torch.equal(n2, npk[a])
+        assert torch.equal(f2, info[a])
+    doa.doa_scan_multi([p.h for p in plans[1:3]], B // 2)     # a subset, fewer frames
+    with pytest.raises(doa.DoaError):
+        doa.doa_scan_multi([p.h for p in plans], B + 1)      # more frames than the plans hold
+    other = doa.Plan(cfg.M, cfg.D, "music", 0.5, max_batch=B)
+    other.run(X)
+    with pytest.raises(doa.DoaError):
+        doa.doa_scan_multi([plans[0].h, other.h], B)          # different grid
+    for p in plans + [other]:
+        p.close()
