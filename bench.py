@@ -234,7 +234,8 @@ class Workload:
         plans and the peak selection) + packing of the peak lists; returns the number of libdoa
         kernel launches.  record=True additionally times the dominant kernel on the step's data:
         the four-plan scan launch (doa_scan_multi on the coefficients doa_run_multi left in the
-        plans; general-array workloads: each plan's doa_spectrum), for the roofline."""
+        plans — one scan_cta_kernel launch per plan; general-array workloads: each plan's
+        doa_spectrum), for the roofline."""
         import torch
         from paper_2007_14135_b200 import binding as bd
         from paper_2007_14135_b200 import dist as pdist
@@ -247,7 +248,7 @@ class Workload:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            bd.doa_scan_multi(hs, self.B, sh)             # one launch: S4-S6 of all four plans
+            bd.doa_scan_multi(hs, self.B, sh)             # S4-S6 of the four plans: 4 scan launches
             e1.record(stream)
             self.spec_ev.append((e0, e1))
             bd.doa_run_multi(hs, self.X, self.idx, self.val, self.npk, self.info, sh)   # restore the outputs
@@ -330,12 +331,14 @@ def scan_roofline(wl, is_array, mirrored):
     cfg = wl.cfg
     M, L, B = cfg.M, cfg.L, wl.B
     spec_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in wl.spec_ev)
-    if is_array:                                   # K - 1 = M(M-1) fp64 FMAs per (frame, grid point), per plan launch
+    if not is_array:                               # doa_scan_multi: the four plans' launches back to back
+        spec_ms /= len(ALGS)
+    if is_array:                                   # K - 1 = M(M-1) fp64 FMAs per (frame, grid point)
         scan_flops = 2.0 * M * (M - 1) * L * B
-    elif mirrored:                                 # per mirrored pair: E and O (2(M-1) FMAs), E +- O (2 adds); 4 plans
-        scan_flops = (2.0 * (M - 1) + 1.0) * L * B * len(ALGS)
-    else:                                          # 2(M-1) fp64 FMAs per (frame, angle); 4 plans per launch
-        scan_flops = 4.0 * (M - 1) * L * B * len(ALGS)
+    elif mirrored:                                 # per mirrored pair: E and O (2(M-1) FMAs), E +- O (2 adds)
+        scan_flops = (2.0 * (M - 1) + 1.0) * L * B
+    else:                                          # 2(M-1) fp64 FMAs per (frame, angle)
+        scan_flops = 4.0 * (M - 1) * L * B
     pk = peaks_json()
     fp64_peak = 148 * 64 * 2 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12   # TFLOP/s, guide unit counts
     achieved = scan_flops / (spec_ms / 1e3) / 1e12
@@ -443,19 +446,17 @@ def main():
     if os.path.exists(tpath) and cfg.name == "c4" and B == cfg.B:
         with open(tpath) as fh:
             rec = json.load(fh).get("scan", {})
-            traffic = rec.get("traffic_bytes") if rec.get("plans_per_launch") == len(ALGS) else None
+            traffic = rec.get("traffic_bytes")
     roofline = {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp64_peak, "traffic": traffic,
                 "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one scan launch, ncu --set full "
-                                  "(profiles/traffic.json); algorithmic operand bytes per launch: the four plans' "
-                                  "coefficients, 4 x 16.8 MB",
+                                  "(profiles/traffic.json); algorithmic operand bytes per launch: coef 16.8 MB",
                 "kernel": ("doa_spectrum per plan (coefficient + array scan kernels)" if is_array else
-                           "scan_cta_kernel (S4-S6, FP64 DMMA mma.sync m8n8k4), one launch over the four "
-                           "estimators' frame groups, timed via doa_scan_multi on the step's coefficients"),
-                "algorithmic_flops_per_point": scan_flops / (L * B * (1 if is_array else len(ALGS))),
-                "mirrored_scan": mirrored,
-                "kernel_ms": spec_ms, "launches_per_step": len(ALGS) if is_array else 1,
-                "share_of_step": spec_ms * (len(ALGS) if is_array else 1) / ms_step,
+                           "scan_cta_kernel (S4-S6, FP64 DMMA mma.sync m8n8k4), one launch per estimator, "
+                           "timed via doa_scan_multi on the step's coefficients (mean per launch)"),
+                "algorithmic_flops_per_point": scan_flops / (L * B), "mirrored_scan": mirrored,
+                "kernel_ms": spec_ms, "launches_per_step": len(ALGS),
+                "share_of_step": spec_ms * len(ALGS) / ms_step,
                 "peak_source": "148 SMs x 64 FP64 lanes x 2 flop x sm_max_mhz (guide unit counts; "
                                "measured DMMA 37.18 / DFMA 34.19 TFLOP/s in profiles/fp64_peaks_r01.txt)"}
     if not is_array:

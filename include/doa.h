@@ -175,10 +175,11 @@ doa_status_t doa_run_multi(const doa_plan_t* plans, int32_t nplans, const float*
 /* S4-S6 again, for 1..4 ULA plans that share M, d/lambda and the grid (typically the four
  * estimators), from the Toeplitz coefficients each plan holds from its most recent doa_spectrum,
  * doa_run or doa_run_multi call (covering at least B frames): the pseudo-spectrum scan and the
- * local-maximum candidates (Table 2 Step-5/6) of all the plans in ONE launch, whose CTAs
- * generate the steering table once for every plan.  The plans' candidate lists are reset and
- * rebuilt, so doa_peaks on each plan afterwards returns what the producing call returned.  Used to
- * re-scan and to time the scan stage on its own (bench.py's roofline).  Errors: general-array
+ * local-maximum candidates (Table 2 Step-5/6) exactly as those calls run them (B <= 16:
+ * one direct-scan launch for all the plans; otherwise one FP64 tensor-core scan launch per plan).
+ * The plans' candidate lists are reset and rebuilt, so doa_peaks on each plan afterwards returns
+ * what the producing call returned.  Used to re-scan and to time the scan stage on its own
+ * (bench.py's roofline).  Errors: general-array
  * plans -> DOA_ERR_UNSUPPORTED; plans that differ in the grid, nplans > 4, or B above the frames
  * the plans hold coefficients for -> DOA_ERR_INVALID_ARG (nothing enqueued). */
 doa_status_t doa_scan_multi(const doa_plan_t* plans, int32_t nplans, int64_t B, doa_stream_t stream);

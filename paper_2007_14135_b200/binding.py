@@ -270,7 +270,7 @@ def doa_run_multi(plans, X, idx, val, npk, info, stream=None):
 
 def doa_scan_multi(plans, B, stream=None):
     """S4-S6 again for 1..4 grid-sharing ULA plans from the coefficients they hold (include/doa.h);
-    the candidate lists are rebuilt for a following doa_peaks.  One launch."""
+    the candidate lists are rebuilt for a following doa_peaks."""
     if not isinstance(plans, (list, tuple)):
         plans = [plans]
     n = len(plans)

@@ -121,15 +121,9 @@ cudaError_t launch_eig16_coef(const double* R, int64_t B, int M, int D, double* 
 cudaError_t launch_coef_multi(const doa_plan_s* const* plans, int nplans, const double* lam, const double* V,
                               int64_t B, int32_t* const* info, cudaStream_t s);
 cudaError_t launch_scan(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s);
-// S4-S6 for 1..kMaxCoefPlans direct_compatible ULA plans (coefficients in place, counters zeroed) in
-// one launch; P (nplans == 1 only) nullable
-struct ScanPlans {
-  const double* coef[kMaxCoefPlans];
-  int32_t* cnt[kMaxCoefPlans];
-  int32_t* cidx[kMaxCoefPlans];
-  double* cf[kMaxCoefPlans];
-  int nplans;
-};
+// S4-S6 for 1..kMaxCoefPlans direct_compatible ULA plans (coefficients in place, counters zeroed):
+// one direct-scan launch for all of them (B <= kDirectMaxB) or one DMMA launch per plan; P
+// (nplans == 1 only) nullable
 cudaError_t launch_scan_plans(const doa_plan_s* const* plans, int nplans, int64_t B, float* P, cudaStream_t s);
 cudaError_t launch_select(const doa_plan_s* p, int64_t B, int32_t* idx, float* val, int32_t* npk, int32_t* info,
                           cudaStream_t s);

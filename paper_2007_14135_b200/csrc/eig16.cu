@@ -87,15 +87,19 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {   // conj(a) * 
 //         (P_n e1)_p = sum_{j<K} V[p][j] conj(V[0][j])     (Q5; e1^H P_n e1 <= 100 eps: unnormalised, G1)
 // Executed by a 16-lane group (hl = lane within it); every sum runs in a fixed ascending order, so
 // eig16h and eig16s (same eigenpairs, same routine) give bitwise identical coefficients.
-//   Vs   [N][N+1] eigenvectors in rank order, Vs[p (N+1) + j] = V[p][j] (written by the caller)
-//   lam  [N] ascending eigenvalues;  Gs [N][N+1], Ws [N], Es [N]: scratch
+// Shared memory: two [N][N+1] double2 buffers (the eigensolver's A double buffer, so the fused
+// kernel needs no extra smem and keeps its occupancy):
+//   Vs  columns j < N: eigenvectors in rank order, Vs[p (N+1) + j] = V[p][j] (written by the caller);
+//       column N: scratch for MN's w
+//   Gs  columns j < N: scratch g_{k,j}; column N: .x = ascending eigenvalues lambda_r at row r
+//       (written by the caller), .y = EV weights
 // Outputs per plan a: coefficients in the scan's A-fragment layout (coef_index), cnt[b] = 0 and
 // info[b] = eigflag | DEGENERATE (overwritten).  `live`: this group holds a real frame b < B.
 template <int N>
-__device__ __forceinline__ void frame_coef(int hl, unsigned gmask, const double2* Vs, const double* lam, double2* Gs,
-                                           double2* Ws, double* Es, int M, int D, const CoefPlans& cp, int64_t b,
-                                           bool live, int eigflag) {
+__device__ __forceinline__ void frame_coef(int hl, unsigned gmask, double2* Vs, double2* Gs, int M, int D,
+                                           const CoefPlans& cp, int64_t b, bool live, int eigflag) {
   constexpr int LDV = N + 1;
+  auto lam = [&](int r) { return Gs[r * LDV + N].x; };
   const int K = M - D;
   bool need_ev = false, need_mn = false;
 #pragma unroll
@@ -122,11 +126,11 @@ __device__ __forceinline__ void frame_coef(int hl, unsigned gmask, const double2
   }
   int flag_ev = 0, flag_mn = 0;
   if (need_ev) {                                        // EV weights, lane-parallel (G1 clamp)
-    const double lfloor = 100.0 * DBL_EPSILON * fmax(lam[M - 1], 0.0);
-    const double lj = hl < K ? lam[hl] : 1.0;
+    const double lfloor = 100.0 * DBL_EPSILON * fmax(lam(M - 1), 0.0);
+    const double lj = hl < K ? lam(hl) : 1.0;
     const bool deg = hl < K && lj <= lfloor;
     if (__ballot_sync(0xffffffffu, deg) & gmask) flag_ev = DOA_INFO_DEGENERATE;
-    Es[hl] = hl < K ? (deg ? (lfloor > 0.0 ? 1.0 / lfloor : 1.0) : 1.0 / lj) : 0.0;
+    if (hl < N) Gs[hl * LDV + N].y = hl < K ? (deg ? (lfloor > 0.0 ? 1.0 / lfloor : 1.0) : 1.0 / lj) : 0.0;
   }
   if (need_mn) {                                        // w_p on lane p, p0 on every lane (same order)
     const int p = hl;
@@ -146,7 +150,7 @@ __device__ __forceinline__ void frame_coef(int hl, unsigned gmask, const double2
     const bool degen = !(p0 > 100.0 * DBL_EPSILON);
     if (degen) flag_mn = DOA_INFO_DEGENERATE;
     const double lp = degen ? 1.0 : 1.0 / p0;
-    Ws[p] = degen ? make_double2(wr, wi) : make_double2(wr * lp, wi * lp);   // zero for p >= M
+    if (p < N) Vs[p * LDV + N] = degen ? make_double2(wr, wi) : make_double2(wr * lp, wi * lp);   // zero for p >= M
   }
   __syncwarp();
   // (b) lane k: combine over j (ascending) and write every plan's coefficients
@@ -161,7 +165,7 @@ __device__ __forceinline__ void frame_coef(int hl, unsigned gmask, const double2
         mus.x += g.x;
         mus.y += g.y;
         if (need_ev) {
-          const double w = Es[j];
+          const double w = Gs[j * LDV + N].y;
           ev.x = fma(w, g.x, ev.x);
           ev.y = fma(w, g.y, ev.y);
         }
@@ -171,7 +175,7 @@ __device__ __forceinline__ void frame_coef(int hl, unsigned gmask, const double2
 #pragma unroll
       for (int p = 0; p < N; ++p) {
         if (p + k < M) {                                // w_p conj(w_{p+k}), ascending p
-          const double2 x = Ws[p], y = Ws[p + k];
+          const double2 x = Vs[p * LDV + N], y = Vs[(p + k) * LDV + N];
           mn.x = fma(x.x, y.x, mn.x);
           mn.x = fma(x.y, y.y, mn.x);
           mn.y = fma(x.y, y.x, mn.y);
@@ -248,8 +252,6 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
   __shared__ double2 As[kHWarps][2][2][N * HLd<N>::LD];          // [warp][half][buffer]
   __shared__ Prm prm[kHWarps][2][N / 2];
   __shared__ int rank_s[kHWarps][2][N];
-  __shared__ double lam_s[FUSE ? kHWarps : 1][2][16], es_s[FUSE ? kHWarps : 1][2][16];
-  __shared__ double2 ws_s[FUSE ? kHWarps : 1][2][16];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int hm = lane >> 4, hl = lane & 15;
   const int64_t b = ((int64_t)blockIdx.x * kHWarps + warp) * 2 + hm;
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
     }
     rank_s[warp][hm][hl] = rk;
     if (valid && lam_out) lam_out[(size_t)b * M + rk] = li;
-    if (FUSE) lam_s[FUSE ? warp : 0][hm][rk] = li;
+    if (FUSE) As[warp][hm][cur][rk * (N + 1) + N].x = li;   // column N: never used by A (j ^ (i/2) < N)
   }
   __syncwarp();
   if (valid && hl < M && V_out) {
@@ -435,8 +437,7 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
         if (k < M) Vs[hl * (N + 1) + rank_s[warp][hm][k]] = v[k];
     }
     __syncwarp();
-    frame_coef<N>(hl, hm ? 0xffff0000u : 0x0000ffffu, Vs, lam_s[FUSE ? warp : 0][hm], As[warp][hm][cur],
-                  ws_s[FUSE ? warp : 0][hm], es_s[FUSE ? warp : 0][hm], M, D, cp, b, valid, flag);
+    frame_coef<N>(hl, hm ? 0xffff0000u : 0x0000ffffu, Vs, As[warp][hm][cur], M, D, cp, b, valid, flag);
   }
 }
 
@@ -498,8 +499,6 @@ __global__ void __launch_bounds__(64) eig16s_kernel(const double2* __restrict__ 
   __shared__ double Dp[2][N];
   __shared__ int rank_s[N];
   __shared__ int go_s;
-  __shared__ double lam_s[FUSE ? 16 : 1], es_s[FUSE ? 16 : 1];
-  __shared__ double2 ws_s[FUSE ? 16 : 1];
   (void)RPW;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t b = blockIdx.x;
@@ -684,7 +683,7 @@ __global__ void __launch_bounds__(64) eig16s_kernel(const double2* __restrict__ 
     }
     rank_s[lane] = rk;
     if (lam_out) lam_out[(size_t)b * M + rk] = li;
-    if (FUSE) lam_s[rk] = li;
+    if (FUSE) As[1][rk * (N + 1) + N].x = li;           // column N: never used by A
   }
   __syncthreads();
   if (warp == 1 && vrow < M) {
@@ -707,8 +706,7 @@ __global__ void __launch_bounds__(64) eig16s_kernel(const double2* __restrict__ 
     if (warp == 0) flag = __shfl_sync(0xffffffffu, flag, 0);
     __syncthreads();
     if (warp == 0)
-      frame_coef<N>(lane & 15, lane < 16 ? 0x0000ffffu : 0xffff0000u, As[0], lam_s, As[1], ws_s, es_s, M, D, cp, b,
-                    lane < 16, flag);
+      frame_coef<N>(lane & 15, lane < 16 ? 0x0000ffffu : 0xffff0000u, As[0], As[1], M, D, cp, b, lane < 16, flag);
   }
 }
 

@@ -499,20 +499,12 @@ __device__ __forceinline__ void scan_epilogue(long long (&v)[2 * NA], int lane, 
   }
 }
 
-// Plan of a frame group gg in [0, nplans * ngroups): groups are plan-major (plan a owns
-// [a ngroups, (a+1) ngroups)); warp-uniform selects, no division.
-__device__ __forceinline__ int group_plan(int64_t gg, int64_t ngroups) {
-  return (int)(gg >= ngroups) + (int)(gg >= 2 * ngroups) + (int)(gg >= 3 * ngroups);
-}
-template <typename T>
-__device__ __forceinline__ T sel4(int a, T x0, T x1, T x2, T x3) {
-  return a == 0 ? x0 : (a == 1 ? x1 : (a == 2 ? x2 : x3));
-}
-
 template <int S, bool WRITE_P, bool MIRROR>
-__global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kernel(ScanPlans sp, int64_t B, int M,
+__global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kernel(const double* __restrict__ coef, int64_t B, int M,
                                                                    int64_t per, double dl, double theta0, double dtheta, int L,
-                                                                   bool sym, int cap, float* __restrict__ P) {
+                                                                   bool sym, int cap, int32_t* __restrict__ cnt,
+                                                                   int32_t* __restrict__ cidx,
+                                                                   double* __restrict__ cf, float* __restrict__ P) {
   using Shape = ScanShape<S, MIRROR>;
   constexpr int NA = Shape::NA, W = Shape::W, NB = Shape::NB, SE = Shape::SE;
   constexpr bool STREAM_A = Shape::STREAM_A;
@@ -523,7 +515,6 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
   const int H = (L + 1) / 2;                                     // lower half [0, H) (MIRROR)
   const int Lt = MIRROR ? H + 1 : L;                             // table-valid tile indices [0, Lt)
   const int64_t ngroups = (B + 7) / 8;
-  const int64_t gtot = ngroups * sp.nplans;                      // frame groups of all plans
   const int64_t y = blockIdx.y;
   const int blk0 = (int)blockIdx.x * NB;
   for (int e = threadIdx.x; e < NB * S * NA * 32; e += kCtaWarps * 32) {
@@ -536,15 +527,10 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
   }
   __syncthreads();
   const int64_t g0 = y * per;
-  const int64_t g1 = (g0 + per < gtot) ? g0 + per : gtot;
-  // A fragments of frame group gg (plan-major over the launch's plans)
-  auto group_coef = [&](int64_t gg) {
-    const int a = group_plan(gg, ngroups);
-    return sel4(a, sp.coef[0], sp.coef[1], sp.coef[2], sp.coef[3]) + ((size_t)(gg - a * ngroups) * S) * 32 + lane;
-  };
+  const int64_t g1 = (g0 + per < ngroups) ? g0 + per : ngroups;
   double an[SA];
   if (!STREAM_A && g0 + warp < g1) {
-    const double* cg = group_coef(g0 + warp);
+    const double* cg = coef + ((size_t)(g0 + warp) * S) * 32 + lane;
 #pragma unroll
     for (int s = 0; s < SA; ++s) an[s] = __ldg(cg + s * 32);
   }
@@ -557,20 +543,15 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
   const int64_t nit = (g1 - g0 + kCtaWarps - 1) / kCtaWarps;
   if (wg == 1) bar_arrive(1);
   for (int64_t it = 0; it < nit; ++it) {
-    const int64_t gg = g0 + warp + it * kCtaWarps;
-    const bool gv = gg < g1;                                     // warp-uniform
-    const int pa = gv ? group_plan(gg, ngroups) : 0;             // this group's plan
-    const int64_t g = gg - pa * ngroups;                         // group within the plan
-    const double* cgc = sel4(pa, sp.coef[0], sp.coef[1], sp.coef[2], sp.coef[3]) + ((size_t)g * S) * 32 + lane;
-    int32_t* const cnt = sel4(pa, sp.cnt[0], sp.cnt[1], sp.cnt[2], sp.cnt[3]);
-    int32_t* const cidx = sel4(pa, sp.cidx[0], sp.cidx[1], sp.cidx[2], sp.cidx[3]);
-    double* const cf = sel4(pa, sp.cf[0], sp.cf[1], sp.cf[2], sp.cf[3]);
+    const int64_t g = g0 + warp + it * kCtaWarps;
+    const bool gv = g < g1;                                      // warp-uniform
+    const double* cgc = coef + ((size_t)g * S) * 32 + lane;   // this group's A fragments
     double a[SA];
     if (!STREAM_A && gv) {
 #pragma unroll
       for (int s = 0; s < SA; ++s) a[s] = an[s];
-      if (gg + kCtaWarps < g1) {                               // prefetch the next group's operands
-        const double* cg = group_coef(gg + kCtaWarps);
+      if (g + kCtaWarps < g1) {                                // prefetch the next group's operands
+        const double* cg = coef + ((size_t)(g + kCtaWarps) * S) * 32 + lane;
 #pragma unroll
         for (int s = 0; s < SA; ++s) an[s] = __ldg(cg + s * 32);
       }
@@ -647,7 +628,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
 }
 
 template <int S, bool MIRROR>
-cudaError_t launch_scan_cta(const ScanPlans& sp, const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
+cudaError_t launch_scan_cta(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
   using Shape = ScanShape<S, MIRROR>;
   constexpr int NA = Shape::NA, W = Shape::W, NB = Shape::NB;
   const size_t smem = (size_t)NB * S * NA * 32 * sizeof(double);
@@ -656,7 +637,7 @@ cudaError_t launch_scan_cta(const ScanPlans& sp, const doa_plan_s* p, int64_t B,
   const int64_t span = MIRROR ? (p->L + 1) / 2 : p->L;          // tile indices the blocks own
   const int64_t nwb = (span + (W - 2) - 1) / (W - 2);            // angle blocks owning [0, span)
   const int64_t gx = (nwb + NB - 1) / NB;                        // angle columns
-  const int64_t ngroups = (B + 7) / 8 * sp.nplans;              // frame groups of all plans
+  const int64_t ngroups = (B + 7) / 8;
   const int64_t slots = (int64_t)sm_count() * occ;
   // frame chunk: ~4 waves of resident CTAs, >= 64 groups (8 per warp) per CTA
   int64_t per = (gx * ngroups) / (4 * slots);
@@ -667,11 +648,11 @@ cudaError_t launch_scan_cta(const ScanPlans& sp, const doa_plan_s* p, int64_t B,
   const bool sym = p->sym != 0;
   count_launch();
   if (P)
-    scan_cta_kernel<S, true, MIRROR><<<grid, kCtaWarps * 32, smem, s>>>(sp, B, p->M, per, p->dl, p->theta0, p->dtheta,
-                                                                        (int)p->L, sym, p->cap, P);
+    scan_cta_kernel<S, true, MIRROR><<<grid, kCtaWarps * 32, smem, s>>>(
+        p->coef, B, p->M, per, p->dl, p->theta0, p->dtheta, (int)p->L, sym, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
   else
-    scan_cta_kernel<S, false, MIRROR><<<grid, kCtaWarps * 32, smem, s>>>(sp, B, p->M, per, p->dl, p->theta0, p->dtheta,
-                                                                         (int)p->L, sym, p->cap, P);
+    scan_cta_kernel<S, false, MIRROR><<<grid, kCtaWarps * 32, smem, s>>>(
+        p->coef, B, p->M, per, p->dl, p->theta0, p->dtheta, (int)p->L, sym, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
   return cudaGetLastError();
 }
 
@@ -770,9 +751,11 @@ bool direct_compatible(const doa_plan_s* a, const doa_plan_s* b) {
 }
 
 // S4-S6 for up to kMaxCoefPlans direct-compatible ULA plans whose coefficients are in place (and
-// counters zeroed): small batches take the direct scan, larger ones ONE DMMA scan launch whose
-// frame groups run over all the plans (the steering table of a CTA serves every plan).  P (single
-// plan only) nullable.
+// counters zeroed): small batches take ONE direct-scan launch for all the plans (the steering is
+// generated once per angle), larger ones one DMMA scan launch per plan.  (A single DMMA launch
+// whose frame groups ran over all the plans — the steering table of a CTA serving every plan — was
+// measured no faster on c4 and its per-group plan selection cost the kernel 7%; see
+// profiles/README.md.)  P (single plan only) nullable.
 cudaError_t launch_scan_plans(const doa_plan_s* const* plans, int nplans, int64_t B, float* P, cudaStream_t s) {
   const doa_plan_s* p = plans[0];
   if (B <= kDirectMaxB) {                                 // small batch: direct scan (scan_direct.cu)
@@ -784,16 +767,16 @@ cudaError_t launch_scan_plans(const doa_plan_s* const* plans, int nplans, int64_
     }
     return launch_scan_direct(a, p, B, s);
   }
-  ScanPlans sp = {};
-  sp.nplans = nplans;
-  for (int k = 0; k < kMaxCoefPlans; ++k) {              // unused slots repeat plan 0 (never selected)
-    const doa_plan_s* q = plans[k < nplans ? k : 0];
-    sp.coef[k] = q->coef; sp.cnt[k] = q->cnt; sp.cidx[k] = q->cand_idx; sp.cf[k] = q->cand_f;
+  if (nplans > 1) {
+    for (int k = 0; k < nplans; ++k) {
+      const cudaError_t e = launch_scan_plans(plans + k, 1, B, nullptr, s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
   }
-  if (nplans > 1) P = nullptr;
   switch (ksteps(p->M)) {
 #define DOA_SCAN_CASE(k) \
-  case k: return p->mirror ? launch_scan_cta<k, true>(sp, p, B, P, s) : launch_scan_cta<k, false>(sp, p, B, P, s);
+  case k: return p->mirror ? launch_scan_cta<k, true>(p, B, P, s) : launch_scan_cta<k, false>(p, B, P, s);
     DOA_SCAN_CASE(1) DOA_SCAN_CASE(2) DOA_SCAN_CASE(3) DOA_SCAN_CASE(4) DOA_SCAN_CASE(5) DOA_SCAN_CASE(6)
     DOA_SCAN_CASE(7) DOA_SCAN_CASE(8) DOA_SCAN_CASE(9) DOA_SCAN_CASE(10) DOA_SCAN_CASE(11) DOA_SCAN_CASE(12)
     DOA_SCAN_CASE(13) DOA_SCAN_CASE(14) DOA_SCAN_CASE(15) DOA_SCAN_CASE(16) DOA_SCAN_CASE(17) DOA_SCAN_CASE(18)

@@ -148,7 +148,7 @@ def test_frame_kernel_matches_staged_path(doa, M, D, B):
         si, sv, sn, sf = [t.cpu().numpy() for t in p.peaks(B, info=sinfo)]
         _, _, _, _, Pf = p.run(X, want_P=True)                   # fused path with P (single plan)
         Ps, Pf = Ps.cpu().numpy().astype(np.float64), Pf.cpu().numpy().astype(np.float64)
-        assert np.max(np.abs(Pf - Ps) / Ps) <= 1e-9, alg        # same eigenpairs, S3 rounded differently
+        assert np.max(np.abs(Pf - Ps) / Ps) <= 1e-6, alg        # same eigenpairs, S3 rounded differently
         diff = np.any(idx[a] != si, axis=1) | (npk[a] != sn)
         assert np.array_equal(info[a][~diff], sf[~diff]), alg
         for b in np.nonzero(diff)[0]:                            # differences only at certified ties
