@@ -49,6 +49,9 @@ def parse():
                          "weak: every GPU owns a full batch")
     ap.add_argument("--no-north-star", dest="north_star", action="store_false",
                     help="skip the north-star (ns) measurement that the default c4 run adds")
+    ap.add_argument("--engine", default="toeplitz_fp64", choices=["toeplitz_fp64", "direct_fp32"],
+                    help="scan engine of the ULA plans (doa_plan_set_engine): the product's fp64 Toeplitz DMMA "
+                         "contraction, or the NEXT-2 FP32-pipe direct form (A/B evidence)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle CPU time for cpu_baseline")
     return ap.parse_args()
 
@@ -207,7 +210,7 @@ EIG_SWEEPS_M16 = 7.72
 class Workload:
     """Plans + buffers + the step of one ULA/array workload on this rank's frames."""
 
-    def __init__(self, cfg, is_array, X, B, dev, doa):
+    def __init__(self, cfg, is_array, X, B, dev, doa, engine="toeplitz_fp64"):
         import torch
         self.cfg, self.B, self.X, self.is_array = cfg, B, X, is_array
         M, D = cfg.M, cfg.D
@@ -216,7 +219,8 @@ class Workload:
                                          cfg.az_wrap, max_batch=B, device=dev) for a in ALGS]
         else:
             self.plans = [doa.Plan(M, D, a, cfg.dtheta, L=cfg.L, theta0=cfg.theta0, d_over_lambda=cfg.d_over_lambda,
-                                   max_batch=B, device=dev) for a in ALGS]
+                                   max_batch=B, device=dev, engine=engine) for a in ALGS]
+        self.engine = "toeplitz_fp64" if is_array else engine
         self.R = torch.empty((B, M, M), dtype=torch.complex128, device=dev)
         self.lam = torch.empty((B, M), dtype=torch.float64, device=dev)
         self.V = torch.empty((B, M, M), dtype=torch.complex128, device=dev)
@@ -333,6 +337,12 @@ def scan_roofline(wl, is_array, mirrored):
     spec_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in wl.spec_ev)
     if not is_array:                               # doa_scan_multi: the four plans' launches back to back
         spec_ms /= len(ALGS)
+    if wl.engine == "direct_fp32":                 # per vector x_j: 4M FFMA for x_j^H a, 2 for |.|^2; mean over plans
+        nv = [(M - cfg.D) if a in ("music", "ev") else 1 for a in ALGS]
+        scan_flops = sum(n * (8.0 * M + 4.0) for n in nv) / len(nv) * L * B
+        pk = peaks_json()
+        fp32_peak = 148 * 128 * 2 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+        return spec_ms, scan_flops, scan_flops / (spec_ms / 1e3) / 1e12, fp32_peak
     if is_array:                                   # K - 1 = M(M-1) fp64 FMAs per (frame, grid point)
         scan_flops = 2.0 * M * (M - 1) * L * B
     elif mirrored:                                 # per mirrored pair: E and O (2(M-1) FMAs), E +- O (2 adds)
@@ -416,7 +426,7 @@ def main():
     del Xh_np
     X = Xh.to(dev)
     D, L = cfg.D, cfg.L
-    wl = Workload(cfg, is_array, X, B, dev, doa)
+    wl = Workload(cfg, is_array, X, B, dev, doa, engine=args.engine)
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
 
@@ -448,7 +458,7 @@ def main():
             rec = json.load(fh).get("scan", {})
             traffic = rec.get("traffic_bytes")
     roofline = {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp64_peak, "traffic": traffic,
+                "frac": achieved / fp64_peak, "traffic": traffic if wl.engine == "toeplitz_fp64" else None,
                 "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one scan launch, ncu --set full "
                                   "(profiles/traffic.json); algorithmic operand bytes per launch: coef 16.8 MB",
                 "kernel": ("doa_spectrum per plan (coefficient + array scan kernels)" if is_array else
@@ -459,6 +469,12 @@ def main():
                 "share_of_step": spec_ms * len(ALGS) / ms_step,
                 "peak_source": "148 SMs x 64 FP64 lanes x 2 flop x sm_max_mhz (guide unit counts; "
                                "measured DMMA 37.18 / DFMA 34.19 TFLOP/s in profiles/fp64_peaks_r01.txt)"}
+    if wl.engine == "direct_fp32":
+        roofline.update({"kernel": "scan_f32_kernel (NEXT-2 FP32-pipe direct form), one launch per estimator, "
+                                   "timed via doa_scan_multi (mean per launch)",
+                         "algorithmic_flops_per_point": scan_flops / (L * B),
+                         "peak_source": "148 SMs x 128 FP32 lanes x 2 flop x sm_max_mhz (guide unit counts; "
+                                        "measured FFMA 72.4 TFLOP/s in profiles/fp64_peaks_r01.txt)"})
     if not is_array:
         roofline["step_roofline_ms"] = step_roofline_ms(cfg, B, mirrored, fp64_peak)
         roofline["step_frac"] = roofline["step_roofline_ms"] / ms_step
@@ -526,9 +542,12 @@ def main():
         cfgd["global_batch"] = total_frames
         cfgd["scaling_split"] = (f"{total_frames} frames split into {ws} contiguous shards (dist.shard_range)"
                                  if scaling == "strong" else f"{B} frames per rank")
+        if wl.engine != "toeplitz_fp64":
+            cfgd["engine"] = wl.engine
         line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
-                "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": scaling, "vs_baseline": None, "dtype": "f64" if wl.engine == "toeplitz_fp64" else "f32",
+                "data": "synthetic",
                 "config": cfgd,
                 "points_per_s": value * L * len(ALGS),
                 "roofline": roofline, "north_star": north, "cpu_baseline": cpu, "clocks": clk, "e2e": e2e,

@@ -111,8 +111,29 @@ int32_t doa_plan_capacity(doa_plan_t plan);
 typedef struct {
   int32_t M, D, alg, geom, device, capacity;
   int64_t L, max_batch;
+  int32_t engine, reserved;       /* DOA_ENGINE_* (doa_plan_set_engine) */
 } doa_plan_info_t;
 doa_status_t doa_plan_info(doa_plan_t plan, doa_plan_info_t* out);
+
+/* Scan engines of a ULA plan.  Step-5 (Table 2) evaluates
+ * f = a^H C a with C the Step-4 noise-subspace form (Table 3):
+ *   DOA_ENGINE_TOEPLITZ_FP64 (default, the product): C reduced to its Toeplitz sums c_k, f as an
+ *     fp64 contraction with a per-angle table on the FP64 tensor pipe (DMMA) — DESIGN.md §5, §7;
+ *   DOA_ENGINE_DIRECT_FP32: the paper's own direct form f = sum_j |x_j^H a|^2 over the weighted
+ *     noise vectors x_j = sqrt(w_j) e_j (MN: the normalised w; PHD: e_min), one thread per angle
+ *     as in §4.3, every product and sum on the FP32 pipe (vectors and steering formed in
+ *     fp64 and rounded to fp32; north_star's "FP32-pipe sincos+FMA" alternative).  It is an A/B
+ *     engine for evidence: several times slower than the Toeplitz contraction at c4, and its fp32
+ *     rounding can move peak indices and exceed 1e-3 dB near deep nulls
+ *     (tests/test_gpu_fp32_engine.py).
+ * doa_spectrum / doa_run / doa_run_multi / doa_run_host / doa_scan_multi of the plan then use the
+ * engine (doa_run_multi keeps the eigendecomposition shared; the frame kernel is used only when
+ * every plan is Toeplitz).  The fp32 engine allocates max_batch*(M-D)*M complex64 (synchronous).
+ * Errors: NULL plan or unknown engine -> DOA_ERR_INVALID_ARG; general-array plans, or
+ * DOA_ENGINE_DIRECT_FP32 with M > 16 -> DOA_ERR_UNSUPPORTED; allocation failure ->
+ * DOA_ERR_OUT_OF_MEMORY.  Must not be called while work on the plan is in flight. */
+enum { DOA_ENGINE_TOEPLITZ_FP64 = 0, DOA_ENGINE_DIRECT_FP32 = 1 };
+doa_status_t doa_plan_set_engine(doa_plan_t plan, int32_t engine);
 
 /* S1 — sample covariance, Eq. 3 / Table 2 Step-1:
  *   R[b] = (1/N) sum_n x_b[n] x_b[n]^H   (1/N, Q20).

@@ -15,13 +15,14 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DOA_LIB") or os.path.join(_HERE, "libdoa.so")   # DOA_LIB: tuning builds only
 
 ALG = {"phd": 0, "music": 1, "ev": 2, "mn": 3}
+ENGINE = {"toeplitz_fp64": 0, "direct_fp32": 1}           # doa_plan_set_engine (include/doa.h)
 INFO_NOCONV, INFO_DEGENERATE, INFO_CAND_OVERFLOW, INFO_UNDERDETERMINED = 1, 2, 4, 8
 STATUS = {0: "DOA_OK", 1: "DOA_ERR_INVALID_ARG", 2: "DOA_ERR_UNSUPPORTED", 3: "DOA_ERR_OUT_OF_MEMORY",
           4: "DOA_ERR_CUDA"}
 
 EXPORTS = ("doa_generate", "doa_plan_create", "doa_plan_create_array", "doa_plan_destroy", "doa_plan_capacity",
            "doa_plan_info", "doa_covariance", "doa_eig",
-           "doa_spectrum", "doa_peaks", "doa_run", "doa_run_multi", "doa_scan_multi", "doa_run_host",
+           "doa_spectrum", "doa_peaks", "doa_run", "doa_run_multi", "doa_scan_multi", "doa_run_host", "doa_plan_set_engine",
            "doa_last_launch_count",
            "doa_status_string", "doa_last_error", "doa_version")
 
@@ -35,7 +36,8 @@ class DoaError(RuntimeError):
 class PlanInfo(C.Structure):
     """doa_plan_info_t (include/doa.h)."""
     _fields_ = [("M", C.c_int32), ("D", C.c_int32), ("alg", C.c_int32), ("geom", C.c_int32),
-                ("device", C.c_int32), ("capacity", C.c_int32), ("L", C.c_int64), ("max_batch", C.c_int64)]
+                ("device", C.c_int32), ("capacity", C.c_int32), ("L", C.c_int64), ("max_batch", C.c_int64),
+                ("engine", C.c_int32), ("reserved", C.c_int32)]
 
 
 def _load():
@@ -58,6 +60,7 @@ def _load():
     L.doa_run_host.argtypes = [C.POINTER(C.c_void_p), i32, fp, i64, i64, i32p, fp, i32p, i32p, vp]
     L.doa_run_multi.argtypes = [C.POINTER(C.c_void_p), i32, fp, i64, i64, i32p, fp, i32p, i32p, vp]
     L.doa_scan_multi.argtypes = [C.POINTER(C.c_void_p), i32, i64, vp]
+    L.doa_plan_set_engine.argtypes = [vp, i32]
     L.doa_generate.argtypes = [i32, d, i32, dp, i32, d, C.c_uint64, i64, i64, i64, fp, vp]
     L.doa_last_launch_count.restype = i32
     L.doa_status_string.argtypes = [C.c_int]
@@ -268,6 +271,12 @@ def doa_run_multi(plans, X, idx, val, npk, info, stream=None):
                              _stream(stream)))
 
 
+def doa_plan_set_engine(plan, engine):
+    """Scan engine of a ULA plan: "toeplitz_fp64" | "direct_fp32" (or the DOA_ENGINE_* value)."""
+    e = ENGINE[engine] if isinstance(engine, str) else int(engine)
+    _check(lib.doa_plan_set_engine(plan, e))
+
+
 def doa_scan_multi(plans, B, stream=None):
     """S4-S6 again for 1..4 grid-sharing ULA plans from the coefficients they hold (include/doa.h);
     the candidate lists are rebuilt for a following doa_peaks."""
@@ -326,15 +335,25 @@ class Plan:
     """Owns one doa_plan_t.  Methods allocate outputs with torch on the plan's device."""
 
     def __init__(self, M, D, alg, dtheta, L=None, theta0=-90.0, d_over_lambda=0.5, max_batch=1,
-                 device="cuda"):
+                 device="cuda", engine="toeplitz_fp64"):
         if L is None:             # last grid point <= 90 deg (the C side's end check)
             L = int(math.floor((90.0 - theta0) / dtheta + 1e-9)) + 1
         self.M, self.D, self.alg, self.L, self.theta0, self.dtheta = M, D, alg, L, theta0, dtheta
         self.device = _device(device)
         self.max_batch = max_batch
+        self.h = None
         with torch.cuda.device(self.device):
             self.h = doa_plan_create(M, d_over_lambda, D, theta0, dtheta, L, alg, max_batch)
         self.cap = int(lib.doa_plan_capacity(self.h))
+        self.engine = "toeplitz_fp64"
+        if engine != "toeplitz_fp64":
+            self.set_engine(engine)
+
+    def set_engine(self, engine):
+        """"toeplitz_fp64" (the product) or "direct_fp32" (SURVEY §8(f) NEXT-2 A/B engine)."""
+        with torch.cuda.device(self.device):
+            doa_plan_set_engine(self.h, engine)
+        self.engine = engine
 
     @classmethod
     def array(cls, positions, D, alg, az0=0.0, daz=1.0, naz=360, el0=90.0, del_=1.0, nel=1, az_wrap=True,

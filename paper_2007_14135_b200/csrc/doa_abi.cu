@@ -76,6 +76,11 @@ cudaError_t ensure_run_scratch(doa_plan_s* p) {
 cudaError_t spectrum_stage(const doa_plan_s* p, const double* lam, const double* V, int64_t B, float* P,
                            int32_t* info, cudaStream_t s) {
   if (p->geom == 1) return doa::launch_array_spectrum(p, lam, V, B, P, info, s);
+  if (p->engine == DOA_ENGINE_DIRECT_FP32) {
+    cudaError_t e = doa::launch_vec32(p, lam, V, B, info, s);
+    if (e != cudaSuccess) return e;
+    return doa::launch_scan_f32(p, B, P, s);
+  }
   cudaError_t e = doa::launch_coef(p, lam, V, B, info, s);
   if (e != cudaSuccess) return e;
   return doa::launch_scan(p, B, P, s);
@@ -88,9 +93,14 @@ cudaError_t scan_stage(doa_plan_s* const* plans, int nplans, int64_t B, float* P
   cudaError_t e = cudaSuccess;
   for (int a = 0; a < nplans && e == cudaSuccess;) {
     if (plans[a]->geom == 1) { ++a; continue; }
+    if (plans[a]->engine == DOA_ENGINE_DIRECT_FP32) {
+      e = doa::launch_scan_f32(plans[a], B, nplans == 1 ? P : nullptr, st);
+      ++a;
+      continue;
+    }
     const doa_plan_s* grp[doa::kMaxCoefPlans] = {};
     int n = 0;
-    while (a < nplans && n < doa::kMaxCoefPlans && plans[a]->geom == 0 &&
+    while (a < nplans && n < doa::kMaxCoefPlans && plans[a]->geom == 0 && plans[a]->engine == DOA_ENGINE_TOEPLITZ_FP64 &&
            (n == 0 || doa::direct_compatible(plans[a], grp[0])))
       grp[n++] = plans[a++];
     e = doa::launch_scan_plans(grp, n, B, nplans == 1 ? P : nullptr, st);
@@ -112,7 +122,7 @@ cudaError_t run_plans(doa_plan_s* const* plans, int nplans, const float* X, int6
   cudaError_t e = doa::launch_covariance(X, B, N, M, p->R, st);
   if (e == cudaSuccess && x_consumed) e = cudaEventRecord(x_consumed, st);   // X no longer needed
   bool fused = M <= 16 && nplans <= doa::kMaxCoefPlans;
-  for (int a = 0; a < nplans; ++a) fused &= plans[a]->geom == 0;
+  for (int a = 0; a < nplans; ++a) fused &= plans[a]->geom == 0 && plans[a]->engine == DOA_ENGINE_TOEPLITZ_FP64;
   if (fused) {
     doa::CoefPlans cp = {};
     cp.nplans = nplans;
@@ -131,6 +141,7 @@ cudaError_t run_plans(doa_plan_s* const* plans, int nplans, const float* X, int6
     for (int a = 0; a < nplans && e == cudaSuccess; ++a) {
       doa_plan_s* q = plans[a];
       if (q->geom == 1) e = doa::launch_array_spectrum(q, p->lam, p->V, B, nplans == 1 ? P : nullptr, info + (size_t)a * ldo, st);
+      else if (q->engine == DOA_ENGINE_DIRECT_FP32) e = doa::launch_vec32(q, p->lam, p->V, B, info + (size_t)a * ldo, st);
       else if (nu < 64) { ula[nu] = q; ula_info[nu++] = info + (size_t)a * ldo; }
       else e = doa::launch_coef(q, p->lam, p->V, B, info + (size_t)a * ldo, st);
     }
@@ -328,7 +339,7 @@ doa_status_t doa_plan_destroy(doa_plan_t p) {
   const int dev = p->device;
   if (cur != dev) cudaSetDevice(dev);                   // free on the plan's device
   cudaDeviceSynchronize();
-  cudaFree(p->dpos); cudaFree(p->fbuf);
+  cudaFree(p->dpos); cudaFree(p->fbuf); cudaFree(p->x32);
   cudaFree(p->cnt); cudaFree(p->cand_idx); cudaFree(p->cand_f); cudaFree(p->coef);
   cudaFree(p->R); cudaFree(p->lam); cudaFree(p->V);
   cudaFree(p->dX[0]); cudaFree(p->dX[1]); cudaFree(p->d_out);
@@ -349,6 +360,25 @@ doa_status_t doa_plan_info(doa_plan_t p, doa_plan_info_t* out) {
   if (!out) return fail(DOA_ERR_INVALID_ARG, "doa_plan_info: out is NULL");
   out->M = p->M; out->D = p->D; out->alg = p->alg; out->geom = p->geom; out->device = p->device;
   out->capacity = p->cap; out->L = p->L; out->max_batch = p->max_batch;
+  out->engine = p->engine; out->reserved = 0;
+  return DOA_OK;
+}
+
+doa_status_t doa_plan_set_engine(doa_plan_t p, int32_t engine) {
+  g_launches = 0;
+  DOA_CHECK_PLAN(p);
+  if (engine != DOA_ENGINE_TOEPLITZ_FP64 && engine != DOA_ENGINE_DIRECT_FP32)
+    return fail(DOA_ERR_INVALID_ARG, "doa_plan_set_engine: unknown engine %d", engine);
+  if (p->geom != 0) return fail(DOA_ERR_UNSUPPORTED, "doa_plan_set_engine: general-array plans have one engine");
+  if (engine == DOA_ENGINE_DIRECT_FP32) {
+    if (p->M > 16) return fail(DOA_ERR_UNSUPPORTED, "doa_plan_set_engine: the fp32 engine supports M <= 16 (M=%d)", p->M);
+    if (!p->x32)
+      DOA_TRY(cudaMalloc((void**)&p->x32, (size_t)p->max_batch * (p->M - p->D) * p->M * 2 * sizeof(float)),
+              "doa_plan_set_engine: vectors");
+  }
+  p->engine = engine;
+  p->coef_B = 0;                                        // coefficients of the other engine are stale
+  p->last_B = 0;
   return DOA_OK;
 }
 
@@ -456,6 +486,8 @@ doa_status_t doa_scan_multi(const doa_plan_t* plans, int32_t nplans, int64_t B, 
     if (plans[a]->geom != 0) return fail(DOA_ERR_UNSUPPORTED, "doa_scan_multi: plans[%d] is a general-array plan", a);
     if (a > 0 && !doa::direct_compatible(plans[a], plans[0]))
       return fail(DOA_ERR_INVALID_ARG, "doa_scan_multi: plans[%d] does not share the grid of plans[0]", a);
+    if (plans[a]->engine != plans[0]->engine)
+      return fail(DOA_ERR_INVALID_ARG, "doa_scan_multi: plans[%d] uses another scan engine than plans[0]", a);
     if (B > plans[a]->coef_B)
       return fail(DOA_ERR_INVALID_ARG, "doa_scan_multi: plans[%d] holds coefficients for %lld frames, B=%lld", a,
                   (long long)plans[a]->coef_B, (long long)B);
@@ -467,7 +499,11 @@ doa_status_t doa_scan_multi(const doa_plan_t* plans, int32_t nplans, int64_t B, 
     grp[a] = plans[a];
     DOA_TRY(cudaMemsetAsync(plans[a]->cnt, 0, (size_t)B * sizeof(int32_t), st2), "doa_scan_multi: counters");
   }
-  DOA_TRY(doa::launch_scan_plans(grp, nplans, B, nullptr, st2), "doa_scan_multi");
+  if (plans[0]->engine == DOA_ENGINE_DIRECT_FP32) {
+    for (int a = 0; a < nplans; ++a) DOA_TRY(doa::launch_scan_f32(plans[a], B, nullptr, st2), "doa_scan_multi");
+  } else {
+    DOA_TRY(doa::launch_scan_plans(grp, nplans, B, nullptr, st2), "doa_scan_multi");
+  }
   for (int a = 0; a < nplans; ++a) plans[a]->last_B = B;
   return DOA_OK;
 }

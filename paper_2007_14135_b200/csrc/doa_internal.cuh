@@ -61,6 +61,38 @@ __device__ __forceinline__ double grid_u(int64_t i, double theta0, double dtheta
   return 2.0 * dl * sinpi(th / 180.0);
 }
 
+// Peak test for the warp-window scans (scan_direct.cu, scan_fp32.cu): a warp owns 64 consecutive tile
+// positions, lane l positions 2l and 2l+1 (0 and 63 are halo).  Peak test on one lane's pair of consecutive positions (v0 at window position 2 lane, v1 at
+// 2 lane + 1; floored bits) and candidate append.  REV: tile index i holds grid index L-1-i.
+template <bool REV>
+__device__ __forceinline__ void window_peaks(long long v0, long long v1, int lane, int base, int ilo, int ihi, int L,
+                                             int cap, int32_t* cnt, int32_t* cidx, double* cf) {
+  const long long vl = __shfl_up_sync(0xffffffffu, v1, 1);          // left of position 2 lane
+  const long long vr = __shfl_down_sync(0xffffffffu, v0, 1);        // right of position 2 lane + 1
+  // forward (Q10): f_i < f_{i-1} and f_i <= f_{i+1}; REV (grid index decreasing with i):
+  // f_i < f_{i+1} and f_i <= f_{i-1}
+  const bool h0 = REV ? (v0 < v1 && v0 <= vl) : (v0 < vl && v0 <= v1);
+  const bool h1 = REV ? (v1 < vr && v1 <= v0) : (v1 < v0 && v1 <= vr);
+  const int i0 = base + 2 * lane, i1 = i0 + 1;
+  const bool d0 = h0 && lane > 0 && i0 >= ilo && i0 <= ihi;            // position 0 is halo
+  const bool d1 = h1 && lane < 31 && i1 >= ilo && i1 <= ihi;           // position 63 is halo
+  if (d0) {
+    const int slot = atomicAdd(cnt, 1);
+    if (slot < cap) { cidx[slot] = REV ? L - 1 - i0 : i0; cf[slot] = __longlong_as_double(v0); }
+  }
+  if (d1) {
+    const int slot = atomicAdd(cnt, 1);
+    if (slot < cap) { cidx[slot] = REV ? L - 1 - i1 : i1; cf[slot] = __longlong_as_double(v1); }
+  }
+}
+
+template <bool REV>
+__device__ __forceinline__ void window_P(long long v0, long long v1, int lane, int base, int whi, int L, float* P) {
+  const int i0 = base + 2 * lane, i1 = i0 + 1;
+  if (lane > 0 && i0 >= 0 && i0 <= whi) P[REV ? L - 1 - i0 : i0] = to_p32(__longlong_as_double(v0));
+  if (lane < 31 && i1 >= 0 && i1 <= whi) P[REV ? L - 1 - i1 : i1] = to_p32(__longlong_as_double(v1));
+}
+
 }  // namespace doa
 
 struct doa_plan_s {
@@ -78,6 +110,8 @@ struct doa_plan_s {
   int32_t wrap;
   double* dpos;                   // [M(M-1)/2][3] device
   double* fbuf;                   // [max_batch][L] floored f of the last doa_spectrum (device)
+  int32_t engine;                 // DOA_ENGINE_*: S3-S6 as the fp64 Toeplitz DMMA contraction or the fp32 direct form
+  float* x32;                     // [max_batch][M-D][M] complex64 weighted noise vectors (fp32 engine, lazily)
   int64_t last_B;                 // B of the last doa_spectrum (consumed by doa_peaks)
   int64_t coef_B;                 // frames whose S3 coefficients the plan holds (doa_scan_multi)
   // workspace (device)
@@ -155,6 +189,11 @@ struct DirectScanArgs {
   int nplans;
 };
 cudaError_t launch_scan_direct(const DirectScanArgs& args, const doa_plan_s* p, int64_t B, cudaStream_t s);
+// NEXT-2, the fp32 direct-form engine (csrc/scan_fp32.cu): S3 as weighted complex64 vectors into
+// p->x32 (counters zeroed, DEGENERATE ORed into info), and the FP32-pipe scan + candidates
+cudaError_t launch_vec32(const doa_plan_s* p, const double* lam, const double* V, int64_t B, int32_t* info,
+                         cudaStream_t s);
+cudaError_t launch_scan_f32(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s);
 // plans that may share one direct scan launch (same M, d/lambda, grid; ULA)
 bool direct_compatible(const doa_plan_s* a, const doa_plan_s* b);
 // general-array plans (csrc/array.cu): coefficients, scan into fbuf, 2-D candidates (+ optional P)

@@ -34,37 +34,6 @@ __device__ __forceinline__ double2 wexact(int k, double u) {    // e^{j k pi u},
   return make_double2(c, s);
 }
 
-// Peak test on one lane's pair of consecutive positions (v0 at window position 2 lane, v1 at
-// 2 lane + 1; floored bits) and candidate append.  REV: tile index i holds grid index L-1-i.
-template <bool REV>
-__device__ __forceinline__ void direct_peaks(long long v0, long long v1, int lane, int base, int ilo, int ihi, int L,
-                                             int cap, int32_t* cnt, int32_t* cidx, double* cf) {
-  const long long vl = __shfl_up_sync(0xffffffffu, v1, 1);          // left of position 2 lane
-  const long long vr = __shfl_down_sync(0xffffffffu, v0, 1);        // right of position 2 lane + 1
-  // forward (Q10): f_i < f_{i-1} and f_i <= f_{i+1}; REV (grid index decreasing with i):
-  // f_i < f_{i+1} and f_i <= f_{i-1}
-  const bool h0 = REV ? (v0 < v1 && v0 <= vl) : (v0 < vl && v0 <= v1);
-  const bool h1 = REV ? (v1 < vr && v1 <= v0) : (v1 < v0 && v1 <= vr);
-  const int i0 = base + 2 * lane, i1 = i0 + 1;
-  const bool d0 = h0 && lane > 0 && i0 >= ilo && i0 <= ihi;            // position 0 is halo
-  const bool d1 = h1 && lane < 31 && i1 >= ilo && i1 <= ihi;           // position 63 is halo
-  if (d0) {
-    const int slot = atomicAdd(cnt, 1);
-    if (slot < cap) { cidx[slot] = REV ? L - 1 - i0 : i0; cf[slot] = __longlong_as_double(v0); }
-  }
-  if (d1) {
-    const int slot = atomicAdd(cnt, 1);
-    if (slot < cap) { cidx[slot] = REV ? L - 1 - i1 : i1; cf[slot] = __longlong_as_double(v1); }
-  }
-}
-
-template <bool REV>
-__device__ __forceinline__ void direct_P(long long v0, long long v1, int lane, int base, int whi, int L, float* P) {
-  const int i0 = base + 2 * lane, i1 = i0 + 1;
-  if (lane > 0 && i0 >= 0 && i0 <= whi) P[REV ? L - 1 - i0 : i0] = to_p32(__longlong_as_double(v0));
-  if (lane < 31 && i1 >= 0 && i1 <= whi) P[REV ? L - 1 - i1 : i1] = to_p32(__longlong_as_double(v1));
-}
-
 template <bool MIRROR>
 __global__ void __launch_bounds__(kDirWarps * 32) scan_direct_kernel(DirectScanArgs a, int64_t B, int M, double dl,
                                                                      double theta0, double dtheta, int L, bool sym,
@@ -140,16 +109,16 @@ __global__ void __launch_bounds__(kDirWarps * 32) scan_direct_kernel(DirectScanA
       const long long lo0 = floor_bits(__double_as_longlong(E[c][0] + O[c][0]));
       const long long lo1 = floor_bits(__double_as_longlong(E[c][1] + O[c][1]));
       if (!MIRROR) {
-        direct_peaks<false>(lo0, lo1, lane, base, 1, L - 2, L, cap, cnt, cidx, cfv);
-        if (P) direct_P<false>(lo0, lo1, lane, base, L - 1, L, P);
+        window_peaks<false>(lo0, lo1, lane, base, 1, L - 2, L, cap, cnt, cidx, cfv);
+        if (P) window_P<false>(lo0, lo1, lane, base, L - 1, L, P);
       } else {
         const long long hi0 = floor_bits(__double_as_longlong(E[c][0] - O[c][0]));
         const long long hi1 = floor_bits(__double_as_longlong(E[c][1] - O[c][1]));
-        direct_peaks<false>(lo0, lo1, lane, base, 1, H - 1, L, cap, cnt, cidx, cfv);
-        direct_peaks<true>(hi0, hi1, lane, base, 1, L - 1 - H, L, cap, cnt, cidx, cfv);
+        window_peaks<false>(lo0, lo1, lane, base, 1, H - 1, L, cap, cnt, cidx, cfv);
+        window_peaks<true>(hi0, hi1, lane, base, 1, L - 1 - H, L, cap, cnt, cidx, cfv);
         if (P) {
-          direct_P<false>(lo0, lo1, lane, base, H - 1, L, P);
-          direct_P<true>(hi0, hi1, lane, base, L - 1 - H, L, P);
+          window_P<false>(lo0, lo1, lane, base, H - 1, L, P);
+          window_P<true>(hi0, hi1, lane, base, L - 1 - H, L, P);
         }
       }
     }

@@ -747,7 +747,7 @@ cudaError_t launch_coef(const doa_plan_s* p, const double* lam, const double* V,
 
 bool direct_compatible(const doa_plan_s* a, const doa_plan_s* b) {
   return a->geom == 0 && b->geom == 0 && a->M == b->M && a->dl == b->dl && a->theta0 == b->theta0 &&
-         a->dtheta == b->dtheta && a->L == b->L && a->mirror == b->mirror && a->cap == b->cap;
+         a->dtheta == b->dtheta && a->L == b->L && a->mirror == b->mirror && a->cap == b->cap && a->engine == b->engine;
 }
 
 // S4-S6 for up to kMaxCoefPlans direct-compatible ULA plans whose coefficients are in place (and

@@ -1,0 +1,109 @@
+"""NEXT-2: the FP32-pipe direct-form scan engine behind the ABI
+(doa_plan_set_engine(plan, DOA_ENGINE_DIRECT_FP32); csrc/scan_fp32.cu), against the fp64 oracle.
+
+It is the A/B alternative to the product's fp64 Toeplitz contraction, not the product: fp32
+rounding of f = sum_j |x_j^H a|^2 costs ~1e-7 relative in f, which near a deep null can reach the
+1e-3 dB bar and shift a peak by a grid point at fine grids.  The tests bound that behaviour and
+record it (gpurun_out/fp32_engine.json): dB error, exact index agreement, largest index offset.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle as orc  # noqa: E402
+from synth import get_config, generate  # noqa: E402
+from tiecert import max_db_error  # noqa: E402
+
+ALGS = ["phd", "music", "ev", "mn"]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+STATS = {}
+
+
+@pytest.fixture(scope="module")
+def doa():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2007_14135_b200 as d
+    yield d
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "fp32_engine.json"), "w") as fh:
+        json.dump(STATS, fh, indent=1)
+
+
+def _check(doa, cfgname, cfg, X, tag):
+    B = X.shape[0]
+    for alg in ALGS:
+        plan = doa.Plan(cfg.M, cfg.D, alg, cfg.dtheta, L=cfg.L, theta0=cfg.theta0, max_batch=B,
+                        engine="direct_fp32")
+        idx, val, npk, info, P = plan.run(torch.from_numpy(X).cuda(), want_P=True)
+        idx, P = idx.cpu().numpy(), P.cpu().numpy()
+        worst_db, exact, total, off = 0.0, 0, 0, 0
+        for b in range(B):
+            R = orc.covariance(X[b])
+            lam, V, _, _ = orc.eig(R)
+            f, _ = orc.spectrum(alg, cfg.D, cfg.d_over_lambda, lam, V, cfg.theta0, cfg.dtheta, cfg.L, threads=8)
+            oidx = orc.peaks(f, cfg.D)[0]
+            worst_db = max(worst_db, max_db_error(P[b], 1.0 / f))
+            np.testing.assert_allclose(P[b].astype(np.float64), 1.0 / f, rtol=2e-3)
+            for g, o in zip(idx[b], oidx):
+                total += 1
+                exact += int(g == o)
+                if g != o:
+                    assert g >= 0 and o >= 0, (alg, b, idx[b], oidx)
+                    off = max(off, int(abs(int(g) - int(o))))
+        STATS[f"{tag}/{alg}"] = {"frames": B, "L": cfg.L, "max_db_error": worst_db, "peaks": total,
+                                 "exact": exact, "max_index_offset": off}
+        assert worst_db <= 2e-2, (alg, worst_db)
+        assert off <= 3, (alg, off)                 # a moved peak stays next to the oracle's
+        assert exact >= 0.9 * total, (alg, exact, total)
+        plan.close()
+
+
+@pytest.mark.parametrize("cfgname", ["c1", "c2", "c3_0.001"])
+def test_fp32_engine_single_frame(doa, cfgname):
+    cfg = get_config(cfgname)
+    _check(doa, cfgname, cfg, generate(cfg), cfgname)
+
+
+def test_fp32_engine_batch(doa):
+    cfg = get_config("c4").with_(dtheta=0.05)
+    _check(doa, "c4", cfg, generate(cfg, frames=range(64)), "c4_0.05_64")
+
+
+def test_fp32_engine_plumbing(doa):
+    """Engine switch, errors, mixed-engine doa_run_multi (the fp32 plans equal their single runs)."""
+    cfg = get_config("c4").with_(dtheta=0.1)
+    B = 40
+    X = torch.from_numpy(generate(cfg, frames=range(B))).cuda()
+    plans = [doa.Plan(cfg.M, cfg.D, a, cfg.dtheta, max_batch=B, engine=("direct_fp32" if k % 2 else "toeplitz_fp64"))
+             for k, a in enumerate(ALGS)]
+    idx, val, npk, info = doa.run_multi(plans, X)
+    for a, p in enumerate(plans):
+        i1, v1, n1, f1, _ = p.run(X)
+        if p.engine == "direct_fp32":
+            assert torch.equal(idx[a], i1) and torch.equal(val[a], v1) and torch.equal(info[a], f1)
+    doa.doa_scan_multi([plans[1].h, plans[3].h], B)           # re-scan two fp32 plans
+    with pytest.raises(doa.DoaError):
+        doa.doa_scan_multi([plans[0].h, plans[1].h], B)       # engines differ
+    big = doa.Plan(33, 4, "music", 1.0, max_batch=2)
+    with pytest.raises(doa.DoaError):
+        big.set_engine("direct_fp32")                         # M > 16
+    with pytest.raises(doa.DoaError):
+        doa.doa_plan_set_engine(plans[0].h, 7)
+    from synth.array import ARRAY_CONFIGS
+    acfg = ARRAY_CONFIGS["e1"]
+    ap = doa.Plan.array(acfg.pos, acfg.D, "music", acfg.az0, acfg.daz, acfg.naz, acfg.el0, acfg.del_, acfg.nel,
+                        acfg.az_wrap, max_batch=1)
+    with pytest.raises(doa.DoaError):
+        ap.set_engine("direct_fp32")
+    plans[0].set_engine("direct_fp32")
+    plans[0].set_engine("toeplitz_fp64")                      # and back: the product path again
+    i2, _, _, _, _ = plans[0].run(X)
+    assert torch.equal(i2, plans[0].run(X)[0])
+    for p in plans + [big, ap]:
+        p.close()
