@@ -21,7 +21,8 @@ namespace doa {
 namespace {
 
 constexpr int kF32Warps = 4;
-constexpr int kF32Frames = 16;     // frames staged per CTA
+constexpr int kF32Vecs = 192;      // frames x vectors staged per CTA (24 KB at M = 16): 16 frames of
+                                   // MUSIC/EV (K = 12), 192 of PHD/MN, so the steering setup amortises
 constexpr int kF32Win = 64;        // tile positions per warp window (62 decided)
 
 // S3 for the fp32 engine: one warp per frame writes the nv weighted vectors x_j (complex64,
@@ -88,11 +89,11 @@ __global__ void __launch_bounds__(kF32Warps * 32, 3) scan_f32_kernel(const float
                                                                   double dtheta, int L, bool sym, int cap,
                                                                   int32_t* __restrict__ cnt,
                                                                   int32_t* __restrict__ cidx, double* __restrict__ cf,
-                                                                  float* __restrict__ P) {
+                                                                  float* __restrict__ P, int fpc) {
   extern __shared__ float4 xs4[];                          // [f][j][MT/2] pairs of complex64
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t b0 = (int64_t)blockIdx.y * kF32Frames;
-  const int nb = (int)(B - b0 < kF32Frames ? B - b0 : kF32Frames);
+  const int64_t b0 = (int64_t)blockIdx.y * fpc;
+  const int nb = (int)(B - b0 < fpc ? B - b0 : fpc);
   float2* xs = reinterpret_cast<float2*>(xs4);
   for (int e = threadIdx.x; e < nb * nv * MT; e += kF32Warps * 32) {
     const int f = e / (nv * MT), r = e - f * (nv * MT), j = r / MT, m = r - (r / MT) * MT;
@@ -163,18 +164,19 @@ cudaError_t launch_scan_f32(const doa_plan_s* p, int64_t B, float* P, cudaStream
   const int K = p->M - p->D;
   const int nv = (p->alg == DOA_ALG_MUSIC || p->alg == DOA_ALG_EV) ? K : 1;
   const int MT = p->M <= 8 ? 8 : 16;
-  const size_t smem = (size_t)kF32Frames * nv * MT * sizeof(float2);
+  const int fpc = kF32Vecs / nv > 0 ? kF32Vecs / nv : 1;
+  const size_t smem = (size_t)fpc * nv * MT * sizeof(float2);
   const int64_t nwin = (p->L + (kF32Win - 2) - 1) / (kF32Win - 2);
   const int64_t gx = (nwin + kF32Warps - 1) / kF32Warps;
-  const dim3 grid((unsigned)gx, (unsigned)((B + kF32Frames - 1) / kF32Frames));
+  const dim3 grid((unsigned)gx, (unsigned)((B + fpc - 1) / fpc));
   const float2* X = reinterpret_cast<const float2*>(p->x32);
   count_launch();
   if (MT == 8)
     scan_f32_kernel<8><<<grid, kF32Warps * 32, smem, s>>>(X, B, K, nv, p->M, p->dl, p->theta0, p->dtheta, (int)p->L,
-                                                          p->sym != 0, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
+                                                          p->sym != 0, p->cap, p->cnt, p->cand_idx, p->cand_f, P, fpc);
   else
     scan_f32_kernel<16><<<grid, kF32Warps * 32, smem, s>>>(X, B, K, nv, p->M, p->dl, p->theta0, p->dtheta, (int)p->L,
-                                                           p->sym != 0, p->cap, p->cnt, p->cand_idx, p->cand_f, P);
+                                                           p->sym != 0, p->cap, p->cnt, p->cand_idx, p->cand_f, P, fpc);
   return cudaGetLastError();
 }
 
