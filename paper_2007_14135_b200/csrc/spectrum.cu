@@ -40,6 +40,10 @@ __device__ __forceinline__ void bar_arrive(int id) {
   if (id == 1) asm volatile("bar.arrive 1, 256;\n" ::: "memory");
   else asm volatile("bar.arrive 2, 256;\n" ::: "memory");
 }
+// Pair-wise variant: warps w and w+4 (same SM sub-partition) hand the DMMA pipe back and forth on
+// their own barriers 1 + 2(w%4) and 2 + 2(w%4) (64 threads), decoupled from the other pairs.
+__device__ __forceinline__ void pbar_sync(int id) { asm volatile("bar.sync %0, 64;\n" :: "r"(id) : "memory"); }
+__device__ __forceinline__ void pbar_arrive(int id) { asm volatile("bar.arrive %0, 64;\n" :: "r"(id) : "memory"); }
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -430,11 +434,28 @@ __host__ __device__ constexpr int tile_pos(int t, int n) { return 2 * NA * (n >>
 // one accumulator set; v[j] (j = 2t + e) is the lane's angle at block position 16q + j.
 // REV: the set holds grid index L-1-i at tile index i (mirrored half).
 // Decided tile indices: interior positions 1..W-2 with i in [ilo, ihi]; P written for i in [0, whi].
+// Deferred candidate store: the lane's first candidate of an epilogue takes its slot with an atomic
+// whose result is consumed only at the lane's next epilogue (or the kernel's end), so the global
+// atomic's round trip overlaps the warp's next DMMA phase instead of stalling the epilogue (and with
+// it the other warp group's turn).  Further candidates of the same epilogue are stored at once.
+struct PendingCand {
+  int slot, b, idx;
+  long long f;
+};
+__device__ __forceinline__ void flush_cand(PendingCand& pc, int cap, int32_t* __restrict__ cidx,
+                                           double* __restrict__ cf) {
+  if (pc.slot >= 0 && pc.slot < cap) {
+    cidx[(size_t)pc.b * cap + pc.slot] = pc.idx;
+    cf[(size_t)pc.b * cap + pc.slot] = __longlong_as_double(pc.f);
+  }
+  pc.slot = -1;
+}
+
 template <int NA, bool WRITE_P, bool REV>
 __device__ __forceinline__ void scan_epilogue(long long (&v)[2 * NA], int lane, int base, int ilo, int ihi, int whi,
                                               int L, int b, bool frame_ok, int cap, int32_t* __restrict__ cnt,
                                               int32_t* __restrict__ cidx, double* __restrict__ cf,
-                                              float* __restrict__ P) {
+                                              float* __restrict__ P, PendingCand& pc) {
   constexpr int W = 8 * NA, R = 2 * NA;
   const int q = lane & 3;
   // Fast path: if every value of the warp's tile is a positive double above the floor and not NaN
@@ -483,6 +504,13 @@ __device__ __forceinline__ void scan_epilogue(long long (&v)[2 * NA], int lane, 
 #pragma unroll
     for (int jj = 0; jj < R; ++jj)
       if (jj == j) f = v[jj];
+    if (pc.slot < 0) {                                     // deferred: stored at the next flush
+      pc.slot = atomicAdd(cnt + b, 1);
+      pc.b = b;
+      pc.idx = REV ? L - 1 - i : i;
+      pc.f = f;
+      continue;
+    }
     const int slot = atomicAdd(cnt + b, 1);
     if (slot < cap) {
       cidx[(size_t)b * cap + slot] = REV ? L - 1 - i : i;
@@ -541,7 +569,14 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
   // chunk's last group still take their turns, without work).
   const int wg = warp >> 2;
   const int64_t nit = (g1 - g0 + kCtaWarps - 1) / kCtaWarps;
+  PendingCand pcand;
+  pcand.slot = -1; pcand.b = 0; pcand.idx = 0; pcand.f = 0;
+#ifdef DOA_SCAN_PAIR_PP
+  const int pbase = 1 + 2 * (warp & 3);
+  if (wg == 1) pbar_arrive(pbase);
+#else
   if (wg == 1) bar_arrive(1);
+#endif
   for (int64_t it = 0; it < nit; ++it) {
     const int64_t g = g0 + warp + it * kCtaWarps;
     const bool gv = g < g1;                                      // warp-uniform
@@ -570,7 +605,11 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
 #pragma unroll
         for (int t = 0; t < (MIRROR ? NA : 1); ++t) { aco[t][0] = 0.0; aco[t][1] = 0.0; }
       }
+#ifdef DOA_SCAN_PAIR_PP
+      pbar_sync(pbase + wg);
+#else
       bar_sync(1 + wg);                         // my group's turn on the pipe
+#endif
       if (gv) {
         if (!MIRROR) {
 #pragma unroll
@@ -599,8 +638,13 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
           }
         }
       }
+#ifdef DOA_SCAN_PAIR_PP
+      pbar_arrive(pbase + 1 - wg);
+#else
       bar_arrive(2 - wg);                       // hand the pipe to the other group
+#endif
       if (!gv) continue;
+      flush_cand(pcand, cap, cidx, cf);                // the previous epilogue's deferred candidate
       if (!MIRROR) {
         long long fi[2 * NA];
 #pragma unroll
@@ -608,7 +652,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
           fi[2 * t] = __double_as_longlong(acc[t][0]);
           fi[2 * t + 1] = __double_as_longlong(acc[t][1]);
         }
-        scan_epilogue<NA, WRITE_P, false>(fi, lane, base, 1, L - 2, L - 1, L, b, frame_ok, cap, cnt, cidx, cf, P);
+        scan_epilogue<NA, WRITE_P, false>(fi, lane, base, 1, L - 2, L - 1, L, b, frame_ok, cap, cnt, cidx, cf, P, pcand);
       } else {
         long long fl[2 * NA], fh[2 * NA];
 #pragma unroll
@@ -619,12 +663,17 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
             fl[2 * t + e] = __double_as_longlong(ev + od);      // f_i          = E + O
             fh[2 * t + e] = __double_as_longlong(ev - od);      // f_{L-1-i}    = E - O
           }
-        scan_epilogue<NA, WRITE_P, false>(fl, lane, base, 1, H - 1, H - 1, L, b, frame_ok, cap, cnt, cidx, cf, P);
-        scan_epilogue<NA, WRITE_P, true>(fh, lane, base, 1, L - 1 - H, L - 1 - H, L, b, frame_ok, cap, cnt, cidx, cf, P);
+        scan_epilogue<NA, WRITE_P, false>(fl, lane, base, 1, H - 1, H - 1, L, b, frame_ok, cap, cnt, cidx, cf, P, pcand);
+        scan_epilogue<NA, WRITE_P, true>(fh, lane, base, 1, L - 1 - H, L - 1 - H, L, b, frame_ok, cap, cnt, cidx, cf, P, pcand);
       }
     }
   }
+  flush_cand(pcand, cap, cidx, cf);
+#ifdef DOA_SCAN_PAIR_PP
+  if (wg == 0) pbar_sync(pbase);
+#else
   if (wg == 0) bar_sync(1);                       // consume the other group's last hand-off
+#endif
 }
 
 template <int S, bool MIRROR>
