@@ -41,12 +41,6 @@ constexpr int kLd = 17;           // smem row stride (double2)
 __device__ constexpr int kBlockOrder[28] = {14, 11, 10, 16, 13, 8, 25, 15, 4, 6, 19, 12, 21, 26,
                                              1, 17, 18, 7, 23, 24, 22, 20, 9, 27, 3, 2, 0, 5};
 
-// eig16h: rotation parameters of one slot pair, padded to 48 bytes so the eight pairs' 16-byte
-// halves fall in distinct shared-memory banks.
-struct __align__(16) Prm {
-  double c, s, er, ei;
-  double pad0, pad1;
-};
 
 // Branch-free reciprocal (square root) for positive normal arguments: MUFU seed (rsqrt/rcp
 // .approx.ftz.f64) + two Newton steps, ~1 ulp.  The library versions add special-case branches
@@ -224,12 +218,6 @@ __device__ __forceinline__ double hsum(double v) {               // sum over a 1
   for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-// half-lane -> block (row-major r < s index): pass 1 lanes 0-15 take entries 0-15, pass 2 lanes
-// 0-11 entries 16-27; from the quarter-warp bank-conflict search (48 wavefronts per round for
-// the block loads / permuted stores + phase 1, against 70 in natural order; ideal 38)
-__device__ constexpr int kHalfOrder[28] = {11, 8, 13, 5, 10, 4, 2, 25, 22, 0, 15, 23, 19, 20,
-                                           21, 18, 12, 7, 14, 27, 26, 9, 17, 16, 1, 3, 6, 24};
-
 // N = 16 or 8 (M <= 8 uses the 8-index round robin: 7 rounds of 4 rotations per sweep).
 template <int N> struct HLd { static constexpr int LD = N == 16 ? kLd : 9; };
 template <int N>
@@ -239,6 +227,56 @@ __host__ __device__ constexpr int cat_next_c(int s, int n) {
 }
 template <int N>
 __device__ __forceinline__ int cat_nextT(int s) { return cat_next_c(s, N); }
+
+// eig16h_kernel<16> shared-memory layout and lane -> block assignment (tools/eig_layout_color.py):
+// off-diagonal element (i < j) of the slot-ordered matrix at slot kOff16[i][j] (16-byte units), the
+// real diagonal as 16 doubles from slot kDiag16.  Every element is read by exactly one
+// (instruction, quarter-warp) group per round and written by exactly one; the slots' bank groups
+// (slot mod 8) are an 8-edge-colouring of the bipartite (load group x store group) multigraph, so
+// every block load, permuted store and phase-1 access is bank-conflict-free.  Lane hl rotates block
+// kLaneBlk16[0][hl] in pass 1 and, for hl < 12, kLaneBlk16[1][hl] in pass 2, which shares its row
+// pair with the pass-1 block (so pass 2 loads one pair's rotation parameters).  Block index =
+// row-major position among the 28 slot-pair blocks r < s.
+__device__ constexpr unsigned char kOff16[16][16] = {
+    {255, 0, 3, 8, 11, 1, 9, 4, 17, 2, 10, 18, 26, 19, 27, 35},
+    {255, 255, 16, 12, 25, 24, 33, 34, 43, 41, 42, 51, 50, 58, 59, 49},
+    {255, 255, 255, 67, 32, 57, 40, 20, 28, 7, 36, 5, 15, 75, 13, 48},
+    {255, 255, 255, 255, 83, 6, 56, 14, 22, 21, 30, 23, 29, 64, 31, 44},
+    {255, 255, 255, 255, 255, 65, 38, 46, 54, 62, 37, 45, 39, 47, 72, 80},
+    {255, 255, 255, 255, 255, 255, 52, 73, 60, 91, 55, 63, 53, 61, 81, 88},
+    {255, 255, 255, 255, 255, 255, 255, 69, 68, 71, 76, 99, 79, 89, 77, 96},
+    {255, 255, 255, 255, 255, 255, 255, 255, 66, 74, 82, 104, 70, 78, 97, 90},
+    {255, 255, 255, 255, 255, 255, 255, 255, 255, 84, 98, 85, 112, 105, 86, 106},
+    {255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 120, 93, 101, 113, 109, 107},
+    {255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 114, 117, 94, 121, 92},
+    {255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 87, 100, 102, 115},
+    {255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 110, 129, 108},
+    {255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 116, 95},
+    {255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 103},
+    {255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255, 255},
+};
+__device__ constexpr signed char kLaneBlk16[2][16] = {
+    {0, 2, 4, 7, 9, 11, 13, 15, 18, 20, 22, 25, 6, 17, 24, 27},
+    {1, 3, 5, 8, 10, 12, 14, 16, 19, 21, 23, 26, -1, -1, -1, -1}};
+constexpr int kDiag16 = 136;
+
+// Element addressing of one matrix buffer: N = 16 the coloured layout above, N = 8 the XOR layout.
+template <int N>
+__device__ __forceinline__ int offslot(int i, int j) {            // i < j
+  if constexpr (N == 16) return kOff16[i][j];
+  else return aidxT<N>(i, j);
+}
+template <int N>
+__device__ __forceinline__ double* diagp(double2* A, int i) {
+  if constexpr (N == 16) return reinterpret_cast<double*>(A + kDiag16) + i;
+  else return &A[aidxT<N>(i, i)].x;
+}
+template <int N>
+__device__ __forceinline__ int blk_of(int hl, int u) {             // lane's block in pass u, -1: none
+  constexpr int NP = N / 2, NBLK = NP * (NP - 1) / 2;
+  if constexpr (N == 16) return kLaneBlk16[u][hl];
+  else return (u == 0 && hl < NBLK) ? hl : -1;
+}
 
 // FUSE: the frame kernel — S3 for the plans in `cp` runs in the epilogue (frame_coef); lam_out /
 // V_out / info may then be NULL (not written).
@@ -250,27 +288,35 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
                                                                              int32_t* __restrict__ info,
                                                                              int D, CoefPlans cp) {
   __shared__ double2 As[kHWarps][2][2][N * HLd<N>::LD];          // [warp][half][buffer]
-  __shared__ Prm prm[kHWarps][2][N / 2];
+  // rotation parameters (c, s) and (Re e, Im e) per slot pair, 16-byte entries: the pairs of a half
+  // sit in distinct bank groups, so every lane -> pair pattern is conflict-free
+  __shared__ double2 pcs[kHWarps][2][N / 2], pee[kHWarps][2][N / 2];
   __shared__ int rank_s[kHWarps][2][N];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int hm = lane >> 4, hl = lane & 15;
   const int64_t b = ((int64_t)blockIdx.x * kHWarps + warp) * 2 + hm;
   const bool valid = b < B;
-  Prm* pm = prm[warp][hm];
+  double2* const Pc = pcs[warp][hm];
+  double2* const Pe = pee[warp][hm];
 
-  // ||R||_F and off(A) are summed in the same order as eig16_kernel's (lane partials over the
-  // element strides of 32, i.e. this half-lane's even and odd strides of 16, added, then the tree),
-  // so both kernels take identical stop decisions and a frame's results do not depend on B.
+  // ||R||_F and off(A) are summed in the same order as eig16s's (lane partials over the element
+  // strides of 32, i.e. this half-lane's even and odd strides of 16, added, then the tree), so both
+  // kernels take identical stop decisions and a frame's results do not depend on B.
   double nrm_e = 0.0, nrm_o = 0.0;
   {
     const double2* Rb = R + (size_t)(valid ? b : 0) * M * M;
+    double2* A0 = As[warp][hm][0];
     for (int e = hl; e < N * N; e += 16) {
       const int i = e / N, j = e % N;
       if (i > j) continue;
       double2 v = make_double2(0.0, 0.0);
       if (valid && j < M) v = Rb[(size_t)i * M + j];
-      if (i == j) v.y = 0.0;
-      As[warp][hm][0][aidxT<N>(i, j)] = v;
+      if (i == j) {
+        v.y = 0.0;
+        *diagp<N>(A0, i) = v.x;
+      } else {
+        A0[offslot<N>(i, j)] = v;
+      }
       const double t = (i == j ? 1.0 : 2.0) * (v.x * v.x + v.y * v.y);
       if ((e / 16) & 1) nrm_o += t; else nrm_e += t;
     }
@@ -281,22 +327,24 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
 #pragma unroll
   for (int k = 0; k < N; ++k) v[k] = make_double2(k == hl ? 1.0 : 0.0, 0.0);
 
-  // off-diagonal blocks per lane: t = hl (+ 16) < NBLK, row-major (r < s) order
-  constexpr int NP = N / 2, NBLK = NP * (NP - 1) / 2, BPL = (NBLK + 15) / 16;
-  int rb2[BPL], sb2[BPL], rd[BPL][4], wr[BPL][4], sgm[BPL];
+  // the lane's off-diagonal blocks: pass 0 and (N = 16, hl < 12) pass 1, which shares the row pair
+  constexpr int NP = N / 2;
+  const int blk[2] = {blk_of<N>(hl, 0), blk_of<N>(hl, 1)};
+  const bool has1 = blk[0] >= 0, has2 = blk[1] >= 0;
+  int rb[2], sb[2], rd[2][4], wr[2][4], sgm[2];
 #pragma unroll
-  for (int u = 0; u < BPL; ++u) {
-    int l = hl + 16 * u;
-    l = l < NBLK ? (N == 16 ? kHalfOrder[l] : l) : 0;
-    int rb = 0, sb = 1;
+  for (int u = 0; u < 2; ++u) {
+    int l = blk[u] < 0 ? 0 : blk[u];
+    int r0 = 0, s0 = 1;
     for (int r = 0; r < NP; ++r) {
       const int cntr = NP - 1 - r;
-      if (l < cntr) { rb = r; sb = r + 1 + l; break; }
+      if (l < cntr) { r0 = r; s0 = r + 1 + l; break; }
       l -= cntr;
     }
-    rb2[u] = rb; sb2[u] = sb;
-    const int i0 = 2 * rb, i1 = i0 + 1, j0 = 2 * sb, j1 = j0 + 1;
-    rd[u][0] = aidxT<N>(i0, j0); rd[u][1] = aidxT<N>(i0, j1); rd[u][2] = aidxT<N>(i1, j0); rd[u][3] = aidxT<N>(i1, j1);
+    rb[u] = r0; sb[u] = s0;
+    const int i0 = 2 * r0, i1 = i0 + 1, j0 = 2 * s0, j1 = j0 + 1;
+    rd[u][0] = offslot<N>(i0, j0); rd[u][1] = offslot<N>(i0, j1);
+    rd[u][2] = offslot<N>(i1, j0); rd[u][3] = offslot<N>(i1, j1);
     const int pr[2] = {cat_nextT<N>(i0), cat_nextT<N>(i1)}, pc[2] = {cat_nextT<N>(j0), cat_nextT<N>(j1)};
     int m = 0;
 #pragma unroll
@@ -304,16 +352,32 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int x = pr[a], y = pc[c];
-        wr[u][2 * a + c] = x < y ? aidxT<N>(x, y) : aidxT<N>(y, x);
+        wr[u][2 * a + c] = x < y ? offslot<N>(x, y) : offslot<N>(y, x);
         m |= (x < y ? 0 : 1) << (2 * a + c);
       }
     sgm[u] = m;
   }
-  const bool has2 = hl + 16 < NBLK;
   const int kx = 2 * (hl % NP), ky = kx + 1, px = cat_nextT<N>(kx), py = cat_nextT<N>(ky);
-  const int rxy = aidxT<N>(kx, ky), rxx = aidxT<N>(kx, kx), ryy = aidxT<N>(ky, ky);
-  const int wxx = aidxT<N>(px, px), wyy = aidxT<N>(py, py), wxy = px < py ? aidxT<N>(px, py) : aidxT<N>(py, px);
+  const int rxy = offslot<N>(kx, ky);
+  const int wxy = px < py ? offslot<N>(px, py) : offslot<N>(py, px);
   __syncwarp();
+
+  // One off-diagonal block: B <- J_r^H B J_s (same operations, same order as eig16s)
+  auto rotate_block = [&](const double2* A, double2* An, int u, double2 rcs, double2 ree, double2 scs, double2 see) {
+    const double2 b00 = A[rd[u][0]], b01 = A[rd[u][1]], b10 = A[rd[u][2]], b11 = A[rd[u][3]];
+    const double pc = rcs.x, ps = rcs.y, qc = scs.x, qs = scs.y;
+    const double2 t0 = cmul(see, b01), t1 = cmul(see, b11);
+    const double2 n00 = make_double2(qc * b00.x - qs * t0.x, qc * b00.y - qs * t0.y);
+    const double2 n01 = make_double2(qs * b00.x + qc * t0.x, qs * b00.y + qc * t0.y);
+    const double2 n10 = make_double2(qc * b10.x - qs * t1.x, qc * b10.y - qs * t1.y);
+    const double2 n11 = make_double2(qs * b10.x + qc * t1.x, qs * b10.y + qc * t1.y);
+    const double2 u0 = cmulc(ree, n10), u1 = cmulc(ree, n11);
+    const int m = sgm[u];
+    An[wr[u][0]] = make_double2(pc * n00.x - ps * u0.x, flipb(pc * n00.y - ps * u0.y, m & 1));
+    An[wr[u][1]] = make_double2(pc * n01.x - ps * u1.x, flipb(pc * n01.y - ps * u1.y, (m >> 1) & 1));
+    An[wr[u][2]] = make_double2(ps * n00.x + pc * u0.x, flipb(ps * n00.y + pc * u0.y, (m >> 2) & 1));
+    An[wr[u][3]] = make_double2(ps * n01.x + pc * u1.x, flipb(ps * n01.y + pc * u1.y, (m >> 3) & 1));
+  };
 
   int flag = 0;
   int cur = 0;
@@ -325,7 +389,7 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
       for (int e = hl; e < N * N; e += 16) {
         const int i = e / N, j = e % N;
         if (i < j) {
-          const double2 a = A[aidxT<N>(i, j)];
+          const double2 a = A[offslot<N>(i, j)];
           if ((e / 16) & 1) off_o += a.x * a.x + a.y * a.y; else off_e += a.x * a.x + a.y * a.y;
         }
       }
@@ -336,18 +400,13 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
     if (!__any_sync(0xffffffffu, act)) break;
 #pragma unroll 1
     for (int rnd = 0; rnd < N - 1; ++rnd) {
-      const double2* A = As[warp][hm][cur];
+      double2* A = As[warp][hm][cur];
       double2* An = As[warp][hm][cur ^ 1];
-      {
-        double2 axy = make_double2(1.0, 0.0);
-        double axx = 0.0, ayy = 0.0;
-        if (hl < NP) {
-          axy = A[rxy];
-          axx = A[rxx].x;
-          ayy = A[ryy].x;
-        }
+      if (hl < NP) {                                     // phase 1: rotation of slot pair hl
+        const double2 axy = A[rxy];
+        const double axx = *diagp<N>(A, kx), ayy = *diagp<N>(A, ky);
         const double r2 = axy.x * axy.x + axy.y * axy.y;
-        const bool rot = act && r2 > 1e-300;               // frozen matrices: identity rotations
+        const bool rot = act && r2 > 1e-300;             // frozen matrices: identity rotations
         const double ir = rsqrt_pos(rot ? r2 : 1.0);
         const double rr = r2 * ir;
         const double d = 0.5 * (ayy - axx);
@@ -359,46 +418,28 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
         const double sabs = rr * rsqrt_pos(2.0 * hh * q);
         const double trabs = r2 * rcp_pos(rot ? q : 1.0);
         const double tr = rot ? (d < 0.0 ? -trabs : trabs) : 0.0;
-        Prm p;
-        p.c = rot ? uu * rsqrt_pos(uu) : 1.0;
-        p.s = rot ? (d < 0.0 ? -sabs : sabs) : 0.0;
-        p.er = rot ? axy.x * ir : 1.0;
-        p.ei = rot ? -axy.y * ir : 0.0;
-        if (hl < NP) {
-          pm[hl] = p;
-          An[wxx] = make_double2(axx - tr, 0.0);
-          An[wyy] = make_double2(ayy + tr, 0.0);
-          An[wxy] = act ? make_double2(0.0, 0.0) : A[rxy];   // frozen: keep the element as it is
-        }
+        Pc[hl] = make_double2(rot ? uu * rsqrt_pos(uu) : 1.0, rot ? (d < 0.0 ? -sabs : sabs) : 0.0);
+        Pe[hl] = make_double2(rot ? axy.x * ir : 1.0, rot ? -axy.y * ir : 0.0);
+        *diagp<N>(An, px) = axx - tr;
+        *diagp<N>(An, py) = ayy + tr;
+        An[wxy] = act ? make_double2(0.0, 0.0) : axy;    // frozen: keep the element as it is
       }
       __syncwarp();
-#pragma unroll
-      for (int u = 0; u < BPL; ++u) {
-        if (u == 1 && !has2) break;
-        const Prm pr = pm[rb2[u]], ps = pm[sb2[u]];
-        const double2 b00 = A[rd[u][0]], b01 = A[rd[u][1]], b10 = A[rd[u][2]], b11 = A[rd[u][3]];
-        const double2 es = make_double2(ps.er, ps.ei), er = make_double2(pr.er, pr.ei);
-        const double2 t0 = cmul(es, b01), t1 = cmul(es, b11);
-        const double2 n00 = make_double2(ps.c * b00.x - ps.s * t0.x, ps.c * b00.y - ps.s * t0.y);
-        const double2 n01 = make_double2(ps.s * b00.x + ps.c * t0.x, ps.s * b00.y + ps.c * t0.y);
-        const double2 n10 = make_double2(ps.c * b10.x - ps.s * t1.x, ps.c * b10.y - ps.s * t1.y);
-        const double2 n11 = make_double2(ps.s * b10.x + ps.c * t1.x, ps.s * b10.y + ps.c * t1.y);
-        const double2 u0 = cmulc(er, n10), u1 = cmulc(er, n11);
-        const int m = sgm[u];
-        An[wr[u][0]] = make_double2(pr.c * n00.x - pr.s * u0.x, flipb(pr.c * n00.y - pr.s * u0.y, m & 1));
-        An[wr[u][1]] = make_double2(pr.c * n01.x - pr.s * u1.x, flipb(pr.c * n01.y - pr.s * u1.y, (m >> 1) & 1));
-        An[wr[u][2]] = make_double2(pr.s * n00.x + pr.c * u0.x, flipb(pr.s * n00.y + pr.c * u0.y, (m >> 2) & 1));
-        An[wr[u][3]] = make_double2(pr.s * n01.x + pr.c * u1.x, flipb(pr.s * n01.y + pr.c * u1.y, (m >> 3) & 1));
+      double2 rcs = make_double2(1.0, 0.0), ree = rcs;
+      if (has1) {
+        rcs = Pc[rb[0]]; ree = Pe[rb[0]];
+        rotate_block(A, An, 0, rcs, ree, Pc[sb[0]], Pe[sb[0]]);
       }
+      if (has2) rotate_block(A, An, 1, rcs, ree, Pc[sb[1]], Pe[sb[1]]);   // same row pair as pass 0
       // V <- V J on the lane's row, then the slot permutation (register renaming + moves)
       double2 t[N];
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
-        const Prm p = pm[k];
+        const double2 cs = Pc[k], ee = Pe[k];
         const double2 vx = v[2 * k], vy = v[2 * k + 1];
-        const double2 ey = cmul(make_double2(p.er, p.ei), vy);
-        t[cat_next_c(2 * k, N)] = make_double2(p.c * vx.x - p.s * ey.x, p.c * vx.y - p.s * ey.y);
-        t[cat_next_c(2 * k + 1, N)] = make_double2(p.s * vx.x + p.c * ey.x, p.s * vx.y + p.c * ey.y);
+        const double2 ey = cmul(ee, vy);
+        t[cat_next_c(2 * k, N)] = make_double2(cs.x * vx.x - cs.y * ey.x, cs.x * vx.y - cs.y * ey.y);
+        t[cat_next_c(2 * k + 1, N)] = make_double2(cs.y * vx.x + cs.x * ey.x, cs.y * vx.y + cs.x * ey.y);
       }
 #pragma unroll
       for (int k = 0; k < N; ++k) v[k] = t[k];
@@ -407,17 +448,19 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
     }
   }
 
-  const double2* A = As[warp][hm][cur];
+  double2* A = As[warp][hm][cur];
   if (hl < M) {
-    const double li = A[aidxT<N>(hl, hl)].x;
+    const double li = *diagp<N>(A, hl);
     int rk = 0;
     for (int j = 0; j < M; ++j) {
-      const double lj = A[aidxT<N>(j, j)].x;
+      const double lj = *diagp<N>(A, j);
       rk += (lj < li) || (lj == li && j < hl);
     }
     rank_s[warp][hm][hl] = rk;
     if (valid && lam_out) lam_out[(size_t)b * M + rk] = li;
-    if (FUSE) As[warp][hm][cur][rk * (N + 1) + N].x = li;   // column N: never used by A (j ^ (i/2) < N)
+    // column N of frame_coef's [N][N+1] view of this buffer: off-diagonal slots no longer needed
+    // (N = 16) or never used (N = 8), and never the diagonal being read here (slots kDiag16..+7)
+    if (FUSE) A[rk * (N + 1) + N].x = li;
   }
   __syncwarp();
   if (valid && hl < M && V_out) {
@@ -437,7 +480,7 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
         if (k < M) Vs[hl * (N + 1) + rank_s[warp][hm][k]] = v[k];
     }
     __syncwarp();
-    frame_coef<N>(hl, hm ? 0xffff0000u : 0x0000ffffu, Vs, As[warp][hm][cur], M, D, cp, b, valid, flag);
+    frame_coef<N>(hl, hm ? 0xffff0000u : 0x0000ffffu, Vs, A, M, D, cp, b, valid, flag);
   }
 }
 
