@@ -138,10 +138,95 @@ __global__ void __launch_bounds__(kSplitMax * 32) cov16_split_kernel(const float
   gram_to_r(acc, &part[0][0][0], lane, N, M, R + (size_t)b * M * M);
 }
 
+// Small batches of long frames (B <= kDirectMaxB, N > 256; the single-frame configs C2/C3): the
+// frame's snapshots are spread over SC <= 16 CTAs of 8 warps (32 snapshots per warp up to N = 4096)
+// so that a single frame uses SC SMs instead of one.  Warp w of CTA c accumulates the snapshot range
+// [(8c + w) Nw, (8c + w + 1) Nw); each CTA sums its warps' tiles in warp order and writes one partial
+// Gram to the workspace; the CTA that takes the last ticket of the frame sums the SC partials in CTA
+// order (fixed order: deterministic; the split depends only on N) and writes R.  The ticket is reset
+// for the next call.  Rounds differently from the batched kernels (a different summation order).
+constexpr int kMultiCtas = 16;
+// snapshots per warp: 32 (one 8-k-step batch of loads in flight, gram_tiles' main loop) while
+// 16 CTAs of 8 warps suffice, else the next multiple of 32
+__host__ __device__ inline int64_t cov_multi_chunk(int64_t N) {
+  const int64_t per = (N + kMultiCtas * kSplitMax - 1) / (kMultiCtas * kSplitMax);
+  return per <= 32 ? 32 : (per + 31) / 32 * 32;
+}
+__global__ void __launch_bounds__(kSplitMax * 32) cov16_multi_kernel(const float2* __restrict__ X, int64_t N, int M,
+                                                                    int SC, double* __restrict__ part,
+                                                                    unsigned* __restrict__ ticket,
+                                                                    double2* __restrict__ R) {
+  __shared__ double red[kSplitMax][10][64];
+  __shared__ unsigned last_s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x;
+  const int64_t b = blockIdx.y;
+  const float2* Xb = X + (size_t)b * N * M;
+  const int64_t Nw = cov_multi_chunk(N);
+  int64_t lo = ((int64_t)c * kSplitMax + warp) * Nw, hi = lo + Nw;
+  lo = lo < N ? lo : N;                                   // warps past the end get an empty range
+  hi = hi < N ? hi : N;
+  double acc[10][2];
+  gram_tiles(Xb, lo, hi, M, lane, acc);
+#pragma unroll
+  for (int t = 0; t < 10; ++t) {
+    red[warp][t][2 * lane] = acc[t][0];
+    red[warp][t][2 * lane + 1] = acc[t][1];
+  }
+  __syncthreads();
+  double* pb = part + ((size_t)b * kMultiCtas + c) * 640;
+  for (int e = threadIdx.x; e < 640; e += kSplitMax * 32) {
+    const int t = e / 64, k = e - (e / 64) * 64;
+    double sum = red[0][t][k];
+    for (int w = 1; w < kSplitMax; ++w) sum += red[w][t][k];
+    pb[e] = sum;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last_s = atomicAdd(ticket + b, 1u) == (unsigned)(SC - 1);
+  __syncthreads();
+  if (!last_s) return;
+  __threadfence();
+  const double* p0 = part + (size_t)b * kMultiCtas * 640;
+  double* tot = &red[1][0][0];                           // 640 sums, then red[0] is gram_to_r's G
+  for (int e = threadIdx.x; e < 640; e += kSplitMax * 32) {
+    double v[kMultiCtas];
+#pragma unroll
+    for (int cc = 0; cc < kMultiCtas; ++cc) v[cc] = cc < SC ? __ldcg(p0 + (size_t)cc * 640 + e) : 0.0;
+    double sum = v[0];
+#pragma unroll
+    for (int cc = 1; cc < kMultiCtas; ++cc)
+      if (cc < SC) sum += v[cc];                          // CTA order
+    tot[e] = sum;
+  }
+  __syncthreads();
+  if (warp != 0) return;
+#pragma unroll
+  for (int t = 0; t < 10; ++t) {
+    acc[t][0] = tot[t * 64 + 2 * lane];
+    acc[t][1] = tot[t * 64 + 2 * lane + 1];
+  }
+  if (lane == 0) ticket[b] = 0u;                          // ready for the next call
+  gram_to_r(acc, &red[0][0][0], lane, N, M, R + (size_t)b * M * M);
+}
+
 }  // namespace
 
-cudaError_t launch_cov16(const float* X, int64_t B, int64_t N, int M, double* R, cudaStream_t s) {
+size_t cov_workspace_bytes() {
+  return (size_t)kDirectMaxB * kMultiCtas * 640 * sizeof(double) + (size_t)kDirectMaxB * sizeof(unsigned);
+}
+
+cudaError_t launch_cov16(const float* X, int64_t B, int64_t N, int M, double* R, cudaStream_t s, void* ws) {
   count_launch();
+  if (ws && B <= kDirectMaxB && N > 256) {
+    const int64_t per_cta = cov_multi_chunk(N) * kSplitMax;
+    const int SC = (int)((N + per_cta - 1) / per_cta);
+    double* part = static_cast<double*>(ws);
+    unsigned* ticket = reinterpret_cast<unsigned*>(part + (size_t)kDirectMaxB * kMultiCtas * 640);
+    cov16_multi_kernel<<<dim3((unsigned)SC, (unsigned)B), kSplitMax * 32, 0, s>>>(
+        reinterpret_cast<const float2*>(X), N, M, SC, part, ticket, reinterpret_cast<double2*>(R));
+    return cudaGetLastError();
+  }
   if (N > 256) {
     const int SW = (int)((N + 127) / 128 < kSplitMax ? (N + 127) / 128 : kSplitMax);
     cov16_split_kernel<<<(unsigned)B, SW * 32, 0, s>>>(reinterpret_cast<const float2*>(X), N, M, SW,

@@ -64,9 +64,11 @@ cudaError_t ensure_run_scratch(doa_plan_s* p) {
   cudaError_t e = cudaMalloc((void**)&p->R, B * M * M * 2 * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc((void**)&p->lam, B * M * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc((void**)&p->V, B * M * M * 2 * sizeof(double));
+  if (e == cudaSuccess && M <= 16) e = cudaMalloc(&p->cov_ws, doa::cov_workspace_bytes());
+  if (e == cudaSuccess && p->cov_ws) e = cudaMemset(p->cov_ws, 0, doa::cov_workspace_bytes());   // tickets
   if (e != cudaSuccess) {
-    cudaFree(p->R); cudaFree(p->lam); cudaFree(p->V);
-    p->R = nullptr; p->lam = nullptr; p->V = nullptr;
+    cudaFree(p->R); cudaFree(p->lam); cudaFree(p->V); cudaFree(p->cov_ws);
+    p->R = nullptr; p->lam = nullptr; p->V = nullptr; p->cov_ws = nullptr;
   }
   return e;
 }
@@ -119,7 +121,7 @@ cudaError_t run_plans(doa_plan_s* const* plans, int nplans, const float* X, int6
                       cudaEvent_t x_consumed = nullptr, float* P = nullptr) {
   doa_plan_s* p = plans[0];
   const int M = p->M, D = p->D;
-  cudaError_t e = doa::launch_covariance(X, B, N, M, p->R, st);
+  cudaError_t e = doa::launch_covariance(X, B, N, M, p->R, st, p->cov_ws);
   if (e == cudaSuccess && x_consumed) e = cudaEventRecord(x_consumed, st);   // X no longer needed
   bool fused = M <= 16 && nplans <= doa::kMaxCoefPlans;
   for (int a = 0; a < nplans; ++a) fused &= plans[a]->geom == 0 && plans[a]->engine == DOA_ENGINE_TOEPLITZ_FP64;
@@ -341,7 +343,7 @@ doa_status_t doa_plan_destroy(doa_plan_t p) {
   cudaDeviceSynchronize();
   cudaFree(p->dpos); cudaFree(p->fbuf); cudaFree(p->x32);
   cudaFree(p->cnt); cudaFree(p->cand_idx); cudaFree(p->cand_f); cudaFree(p->coef);
-  cudaFree(p->R); cudaFree(p->lam); cudaFree(p->V);
+  cudaFree(p->R); cudaFree(p->lam); cudaFree(p->V); cudaFree(p->cov_ws);
   cudaFree(p->dX[0]); cudaFree(p->dX[1]); cudaFree(p->d_out);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   for (int k = 0; k < 2; ++k) {

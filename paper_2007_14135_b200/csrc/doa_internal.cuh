@@ -122,6 +122,7 @@ struct doa_plan_s {
   double* R;                      // [max_batch][M][M][2]  doa_run scratch
   double* lam;                    // [max_batch][M]
   double* V;                      // [max_batch][M][M][2]
+  void* cov_ws;                   // small-batch multi-CTA covariance workspace (cov_workspace_bytes)
   // doa_run_host staging (lazily sized on first use)
   float* dX[2];
   size_t dX_bytes;
@@ -135,7 +136,11 @@ namespace doa {
 
 // Launchers (enqueue only; return cudaGetLastError() of the launch).  Each increments the
 // thread-local launch counter.
-cudaError_t launch_covariance(const float* X, int64_t B, int64_t N, int M, double* R, cudaStream_t s);
+// ws: nullable workspace of cov_workspace_bytes() (zero-initialised once) for the small-batch
+// multi-CTA covariance (B <= kDirectMaxB, N > 256, M <= 16); without it the per-frame kernels run
+cudaError_t launch_covariance(const float* X, int64_t B, int64_t N, int M, double* R, cudaStream_t s,
+                              void* ws = nullptr);
+size_t cov_workspace_bytes();
 cudaError_t launch_eig(const double* R, int64_t B, int M, double* lam, double* V, int32_t* info, cudaStream_t s);
 cudaError_t launch_coef(const doa_plan_s* p, const double* lam, const double* V, int64_t B, int32_t* info,
                         cudaStream_t s);

@@ -44,7 +44,9 @@ __device__ constexpr int kBlockOrder[28] = {14, 11, 10, 16, 13, 8, 25, 15, 4, 6,
 
 // Branch-free reciprocal (square root) for positive normal arguments: MUFU seed (rsqrt/rcp
 // .approx.ftz.f64) + two Newton steps, ~1 ulp.  The library versions add special-case branches
-// that cost a third of the rotation-parameter instructions.
+// that cost a third of the rotation-parameter instructions.  The rotation code feeds them
+// unguarded values (a zero pivot gives inf/NaN intermediates) and selects the identity rotation
+// at the end, keeping selects off the latency chain.
 __device__ __forceinline__ double rsqrt_pos(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -386,11 +388,12 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
     {
       const double2* A = As[warp][hm][cur];
       double off_e = 0.0, off_o = 0.0;
-      for (int e = hl; e < N * N; e += 16) {
-        const int i = e / N, j = e % N;
+#pragma unroll
+      for (int it = 0; it < N * N / 16; ++it) {
+        const int e = hl + 16 * it, i = e / N, j = e % N;
         if (i < j) {
           const double2 a = A[offslot<N>(i, j)];
-          if ((e / 16) & 1) off_o += a.x * a.x + a.y * a.y; else off_e += a.x * a.x + a.y * a.y;
+          if (it & 1) off_o += a.x * a.x + a.y * a.y; else off_e += a.x * a.x + a.y * a.y;
         }
       }
       const double off = sqrt(2.0 * hsum(off_e + off_o));
@@ -407,16 +410,16 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
         const double axx = *diagp<N>(A, kx), ayy = *diagp<N>(A, ky);
         const double r2 = axy.x * axy.x + axy.y * axy.y;
         const bool rot = act && r2 > 1e-300;             // frozen matrices: identity rotations
-        const double ir = rsqrt_pos(rot ? r2 : 1.0);
+        const double ir = rsqrt_pos(r2);
         const double rr = r2 * ir;
         const double d = 0.5 * (ayy - axx);
         const double h2 = fma(d, d, r2);
-        const double irh = rsqrt_pos(rot ? h2 : 1.0);
+        const double irh = rsqrt_pos(h2);
         const double hh = h2 * irh;
         const double q = fabs(d) + hh;
         const double uu = 0.5 * q * irh;
         const double sabs = rr * rsqrt_pos(2.0 * hh * q);
-        const double trabs = r2 * rcp_pos(rot ? q : 1.0);
+        const double trabs = r2 * rcp_pos(q);
         const double tr = rot ? (d < 0.0 ? -trabs : trabs) : 0.0;
         Pc[hl] = make_double2(rot ? uu * rsqrt_pos(uu) : 1.0, rot ? (d < 0.0 ? -sabs : sabs) : 0.0);
         Pe[hl] = make_double2(rot ? axy.x * ir : 1.0, rot ? -axy.y * ir : 0.0);
@@ -485,13 +488,14 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
 }
 
 
-// Small-batch variant (latency): one matrix per CTA of two warps, software-pipelined like a
-// systolic array.  Warp 0 owns the 28 off-diagonal blocks (one per lane) and, as "pilot", derives
-// the NEXT round's rotations from the block outputs it has just computed (each next-round pair's
-// off-diagonal element is one of them) and the post-rotation diagonal; warp 1 applies the current
-// round's rotations to V (lane l: row l/2, slot half l%2, 8 complex in registers) at the same
-// time.  One CTA barrier per round, so a round's critical path is one block update plus one
-// rotation-parameter chain.  Same rotation formulas, operation order, stop-rule sums (lanes 0-15
+// Small-batch variant (latency): one matrix per CTA of three warps, software-pipelined like a
+// systolic array.  Warp 0 owns the 28 off-diagonal blocks (one per lane); warp 2 is the "pilot":
+// lane k recomputes (same operations) the rotated element of the block that becomes next-round pair
+// k's off-diagonal element and derives the NEXT round's rotation from it and the post-rotation
+// diagonal; warp 1 applies the current round's rotations to V (lane l: row l/2, slot half l%2, 8
+// complex in registers) at the same time.  One CTA barrier per round, so a round's critical path is
+// one block update plus one rotation-parameter chain, and each warp's instruction stream is short
+// (with the pilot inside warp 0 its stream was the serial sum of both; 74 us per matrix at M = 16).  Same rotation formulas, operation order, stop-rule sums (lanes 0-15
 // of warp 0 reproduce eig16h's partial sums and tree) and slot permutation as eig16h_kernel, so
 // both kernels give bitwise identical eigenpairs (tests/test_gpu_parity.py::
 // test_eig_kernels_bitwise_equal) and a frame's result does not depend on B.
@@ -501,16 +505,16 @@ struct RotP {
 __device__ __forceinline__ RotP rot_params_s(double axx, double ayy, double2 axy) {
   const double r2 = axy.x * axy.x + axy.y * axy.y;
   const bool rot = r2 > 1e-300;                              // a_xy ~ 0: identity rotation
-  const double ir = rsqrt_pos(rot ? r2 : 1.0);
+  const double ir = rsqrt_pos(r2);
   const double rr = r2 * ir;
   const double d = 0.5 * (ayy - axx);
   const double h2 = fma(d, d, r2);
-  const double irh = rsqrt_pos(rot ? h2 : 1.0);
+  const double irh = rsqrt_pos(h2);
   const double hh = h2 * irh;
   const double q = fabs(d) + hh;
   const double uu = 0.5 * q * irh;
-  const double sabs = rr * rsqrt_pos(rot ? 2.0 * hh * q : 1.0);
-  const double trabs = r2 * rcp_pos(rot ? q : 1.0);
+  const double sabs = rr * rsqrt_pos(2.0 * hh * q);
+  const double trabs = r2 * rcp_pos(q);
   RotP p;
   p.tr = rot ? (d < 0.0 ? -trabs : trabs) : 0.0;
   p.c = rot ? uu * rsqrt_pos(uu) : 1.0;
@@ -530,8 +534,15 @@ __device__ __forceinline__ double2 sel2(bool p, double2 a, double2 b) {
   return make_double2(p ? a.x : b.x, p ? a.y : b.y);
 }
 
+constexpr int kSThreads = 96;      // eig16s: warp 0 blocks, warp 1 V, warp 2 pilot
+#ifdef DOA_EIG_TRACE
+__device__ long long g_eig_trace[8 * 512];      // tools/eig16s_trace.cu: clock64 per round and warp
+#define EIG_TRACE(slot) do { if (blockIdx.x == 0 && lane == 0 && rg < 512) g_eig_trace[8 * rg + (slot)] = clock64(); } while (0)
+#else
+#define EIG_TRACE(slot) do { } while (0)
+#endif
 template <int N, bool FUSE>
-__global__ void __launch_bounds__(64) eig16s_kernel(const double2* __restrict__ R, int64_t B, int M,
+__global__ void __launch_bounds__(kSThreads) eig16s_kernel(const double2* __restrict__ R, int64_t B, int M,
                                                     double* __restrict__ lam_out, double2* __restrict__ V_out,
                                                     int32_t* __restrict__ info, int D, CoefPlans cp) {
   constexpr int NP = N / 2, NBLK = NP * (NP - 1) / 2, SPL = N / 2, RPW = 32 / (N / 4) / 2;
@@ -549,7 +560,7 @@ __global__ void __launch_bounds__(64) eig16s_kernel(const double2* __restrict__ 
 
   // ---- load; ||R||_F in eig16h's order (lanes 0-15 of warp 0)
   double nrm_e = 0.0, nrm_o = 0.0;
-  for (int e = tid; e < N * N; e += 64) {
+  for (int e = tid; e < N * N; e += kSThreads) {
     const int i = e / N, j = e % N;
     if (i > j) continue;
     double2 v = make_double2(0.0, 0.0);
@@ -561,30 +572,43 @@ __global__ void __launch_bounds__(64) eig16s_kernel(const double2* __restrict__ 
       As[0][aidxT<N>(i, j)] = v;
     }
   }
-  if (warp == 0 && lane < 16)
-    for (int e = lane; e < N * N; e += 16) {
-      const int i = e / N, j = e % N;
+  __syncthreads();
+  if (warp == 0 && lane < 16) {                        // from the staged copy: loads in flight together
+#pragma unroll
+    for (int it = 0; it < N * N / 16; ++it) {
+      const int e = lane + 16 * it, i = e / N, j = e % N;
       if (i > j) continue;
-      double2 v = make_double2(0.0, 0.0);
-      if (j < M) v = Rb[(size_t)i * M + j];
-      if (i == j) v.y = 0.0;
+      const double2 v = i == j ? make_double2(Dp[1][cat_prev_c(i, N)], 0.0) : As[0][aidxT<N>(i, j)];
       const double t = (i == j ? 1.0 : 2.0) * (v.x * v.x + v.y * v.y);
-      if ((e / 16) & 1) nrm_o += t; else nrm_e += t;
+      if (it & 1) nrm_o += t; else nrm_e += t;
     }
+  }
   double tol = 0.0;
   if (warp == 0) tol = 10.0 * DBL_EPSILON * sqrt(hsum(nrm_e + nrm_o));
-  __syncthreads();
 
-  // ---- per-lane geometry (warp 0: block lane < NBLK, pilot element; warp 1: V)
+  // ---- per-lane geometry (warp 0: block lane < NBLK; warp 1: V; warp 2 lane k < NP: the pilot of
+  // next-round pair k, i.e. the block one of whose rotated elements becomes that pair's a_xy)
   const bool hasb = warp == 0 && lane < NBLK;
-  int rb = 0, sb = 1;
-  {
-    int t = hasb ? (N == 16 ? kBlockOrder[lane] : lane) : 0;
+  auto decode = [&](int t, int& r0, int& s0) {
+    r0 = 0; s0 = 1;
     for (int r = 0; r < NP; ++r) {
       const int cntr = NP - 1 - r;
-      if (t < cntr) { rb = r; sb = r + 1 + t; break; }
+      if (t < cntr) { r0 = r; s0 = r + 1 + t; break; }
       t -= cntr;
     }
+  };
+  int rb = 0, sb = 1;
+  if (warp == 2) {
+    for (int t = 0; t < NBLK; ++t) {
+      int r0, s0;
+      decode(t, r0, s0);
+      for (int e = 0; e < 4; ++e) {
+        const int x = cat_next_c(2 * r0 + (e >> 1), N), y = cat_next_c(2 * s0 + (e & 1), N);
+        if ((x >> 1) == (y >> 1) && (x >> 1) == lane) { rb = r0; sb = s0; }
+      }
+    }
+  } else {
+    decode(hasb ? (N == 16 ? kBlockOrder[lane] : lane) : 0, rb, sb);
   }
   int rdo[4], wro[4], cjm = 0;
   {
@@ -605,7 +629,7 @@ __global__ void __launch_bounds__(64) eig16s_kernel(const double2* __restrict__ 
   for (int e = 0; e < 4; ++e) {
     const int i = 2 * rb + (e >> 1), j = 2 * sb + (e & 1);
     const int x = cat_next_c(i, N), y = cat_next_c(j, N);
-    if (hasb && (x >> 1) == (y >> 1)) {
+    if (warp == 2 && lane < NP && (x >> 1) == (y >> 1)) {
       pil = true; pe = e; pk = x >> 1;
       pxo = (x & 1) ? j : i;
       pyo = (x & 1) ? i : j;
@@ -638,14 +662,16 @@ __global__ void __launch_bounds__(64) eig16s_kernel(const double2* __restrict__ 
     if (warp == 0) {                                   // stop rule, eig16h's summation order
       const double2* A = As[pb];
       double off_e = 0.0, off_o = 0.0;
-      if (lane < 16)
-        for (int e = lane; e < N * N; e += 16) {
-          const int i = e / N, j = e % N;
+      if (lane < 16) {
+#pragma unroll
+        for (int it = 0; it < N * N / 16; ++it) {
+          const int e = lane + 16 * it, i = e / N, j = e % N;
           if (i < j) {
             const double2 a = A[aidxT<N>(i, j)];
-            if ((e / 16) & 1) off_o += a.x * a.x + a.y * a.y; else off_e += a.x * a.x + a.y * a.y;
+            if (it & 1) off_o += a.x * a.x + a.y * a.y; else off_e += a.x * a.x + a.y * a.y;
           }
         }
+      }
       const double off = sqrt(2.0 * hsum(off_e + off_o));
       if (lane == 0) {
         int go = 1;
@@ -658,7 +684,14 @@ __global__ void __launch_bounds__(64) eig16s_kernel(const double2* __restrict__ 
     if (!go_s) break;
 #pragma unroll 1
     for (int rnd = 0; rnd < N - 1; ++rnd) {
-      if (warp == 0) {
+#ifdef DOA_EIG_TRACE
+      const int rg = sweep * (N - 1) + rnd;
+#endif
+      if (warp == 2) EIG_TRACE(0);
+      if (warp == 0 || warp == 2) {
+        // warp 0 rotates the blocks; warp 2 (pilot) recomputes, with the same operations, the one
+        // rotated element that becomes its next-round pair's a_xy and derives that rotation, so the
+        // rotation-parameter chain runs beside the block updates instead of after them
         const double2* A = As[pb];
         double2* An = As[pb ^ 1];
         const double2 rcs = Pcs[pb][rb], ree = Pee[pb][rb], scs = Pcs[pb][sb], see = Pee[pb][sb];
@@ -680,17 +713,19 @@ __global__ void __launch_bounds__(64) eig16s_kernel(const double2* __restrict__ 
           An[wro[2]] = make_double2(o2.x, flipb(o2.y, (cjm >> 2) & 1));
           An[wro[3]] = make_double2(o3.x, flipb(o3.y, (cjm >> 3) & 1));
         }
-        if (lane < NP) An[zpos] = make_double2(0.0, 0.0);          // the zeroed pair elements
+        if (warp == 0 && lane < NP) An[zpos] = make_double2(0.0, 0.0);   // the zeroed pair elements
+        if (warp == 0) EIG_TRACE(2);
         if (pil) {                                                  // next round's rotation
-          const double2 pv = sel2(pe == 0, o0, sel2(pe == 1, o1, sel2(pe == 2, o2, o3)));
+          const double2 pv = sel2(pe >= 2, sel2(pe & 1, o3, o2), sel2(pe & 1, o1, o0));
           const double axx = Dp[pb][pxo], ayy = Dp[pb][pyo];
           const RotP p = rot_params_s(axx, ayy, make_double2(pv.x, flipb(pv.y, pcj)));
+          EIG_TRACE(1);
           Pcs[pb ^ 1][pk] = make_double2(p.c, p.s);
           Pee[pb ^ 1][pk] = make_double2(p.er, p.ei);
           Dp[pb ^ 1][2 * pk] = axx - p.tr;
           Dp[pb ^ 1][2 * pk + 1] = ayy + p.tr;
         }
-      } else if (N == 16 || lane < 16) {
+      } else if (warp == 1 && (N == 16 || lane < 16)) {
         // V <- V J on row vrow, slot half g; then the slot permutation (one complex crosses)
         double2 nv[SPL];
 #pragma unroll
@@ -711,6 +746,7 @@ __global__ void __launch_bounds__(64) eig16s_kernel(const double2* __restrict__ 
           const double2 a1 = s1 < 0 ? recv : nv[s1 < 0 ? 0 : s1];
           v[l] = s0 == s1 ? a0 : sel2(g == 0, a0, a1);
         }
+        EIG_TRACE(3);
       }
       pb ^= 1;
       __syncthreads();
@@ -766,8 +802,8 @@ cudaError_t launch16(const double* R, int64_t B, int M, double* lam, double* V, 
   const double2* R2 = reinterpret_cast<const double2*>(R);
   double2* V2 = reinterpret_cast<double2*>(V);
   if (B < DOA_EIG_HALF_MIN_B) {
-    if (M <= 8) eig16s_kernel<8, FUSE><<<(unsigned)B, 64, 0, s>>>(R2, B, M, lam, V2, info, D, cp);
-    else eig16s_kernel<16, FUSE><<<(unsigned)B, 64, 0, s>>>(R2, B, M, lam, V2, info, D, cp);
+    if (M <= 8) eig16s_kernel<8, FUSE><<<(unsigned)B, kSThreads, 0, s>>>(R2, B, M, lam, V2, info, D, cp);
+    else eig16s_kernel<16, FUSE><<<(unsigned)B, kSThreads, 0, s>>>(R2, B, M, lam, V2, info, D, cp);
     return cudaGetLastError();
   }
   const unsigned g = (unsigned)((B + 2 * kHWarps - 1) / (2 * kHWarps));

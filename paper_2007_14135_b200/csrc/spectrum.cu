@@ -40,10 +40,12 @@ __device__ __forceinline__ void bar_arrive(int id) {
   if (id == 1) asm volatile("bar.arrive 1, 256;\n" ::: "memory");
   else asm volatile("bar.arrive 2, 256;\n" ::: "memory");
 }
-// Pair-wise variant: warps w and w+4 (same SM sub-partition) hand the DMMA pipe back and forth on
-// their own barriers 1 + 2(w%4) and 2 + 2(w%4) (64 threads), decoupled from the other pairs.
+#ifdef DOA_SCAN_PAIR_PP
+// A/B variant (no gain measured): warps w and w+4 (same SM sub-partition) hand the DMMA pipe back
+// and forth on their own barriers 1 + 2(w%4) and 2 + 2(w%4) (64 threads), decoupled from the others.
 __device__ __forceinline__ void pbar_sync(int id) { asm volatile("bar.sync %0, 64;\n" :: "r"(id) : "memory"); }
 __device__ __forceinline__ void pbar_arrive(int id) { asm volatile("bar.arrive %0, 64;\n" :: "r"(id) : "memory"); }
+#endif
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
