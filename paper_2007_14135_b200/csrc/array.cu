@@ -232,6 +232,85 @@ __global__ void peaks2d_kernel(const double* __restrict__ fbuf, int64_t B, int64
   }
 }
 
+// The same 2-D findPeaks on tiles: a CTA takes TA consecutive azimuth rows of one frame (all nel
+// elevations) plus the two neighbouring rows (wrapped when the azimuth wraps), stages them in shared
+// memory once, and tests every core point against its 8 neighbours there — f is read ~(TA+2)/TA
+// times instead of up to 9 times through L1/L2.  Same rule, same candidates (their list order may
+// differ; doa_peaks sorts).  Used when (TA+2) * nel fits the tile (nel <= kPk2MaxNel).
+constexpr int kPk2Vals = 2048;       // core values per tile (TA = kPk2Vals / nel rows)
+constexpr int kPk2MaxNel = 2048;
+__global__ void __launch_bounds__(256) peaks2d_tile_kernel(const double* __restrict__ fbuf, int64_t naz, int64_t nel,
+                                                           int TA, int wrap, int cap, int32_t* __restrict__ cnt,
+                                                           int32_t* __restrict__ cidx, double* __restrict__ cf,
+                                                           float* __restrict__ P) {
+  extern __shared__ double ft[];                       // [TA + 2][nel]: rows ia0-1 .. ia0+TA
+  __shared__ int rowok[2];                             // halo rows present (wrap or inside the grid)
+  const int64_t L = naz * nel;
+  const int64_t b = blockIdx.y;
+  const int64_t ia0 = (int64_t)blockIdx.x * TA;
+  const int nr = (int)(ia0 + TA <= naz ? TA : naz - ia0);   // core rows of this tile
+  const double* fb = fbuf + (size_t)b * L;
+  {                                                    // stage rows ia0-1 .. ia0+nr (int32 walk, no divisions)
+    const int nelI = (int)nel, nvals = (nr + 2) * nelI;
+    const int sr = (int)(blockDim.x / nelI), se = (int)(blockDim.x - sr * nelI);
+    int row = (int)(threadIdx.x / nelI), ie = (int)(threadIdx.x - (threadIdx.x / nelI) * nelI);
+    for (int e = threadIdx.x; e < nvals; e += blockDim.x, row += sr, ie += se) {
+      if (ie >= nelI) { ie -= nelI; ++row; }
+      int64_t ja = ia0 - 1 + row;
+      bool ok = ja >= 0 && ja < naz;
+      if (!ok && wrap) { ja = ja < 0 ? ja + naz : ja - naz; ok = true; }
+      ft[e] = ok ? __ldcs(fb + ja * nel + ie) : 0.0;      // f is read once: streaming load
+    }
+  }
+  if (threadIdx.x < 2) {
+    const int64_t ja = threadIdx.x == 0 ? ia0 - 1 : ia0 + nr;
+    rowok[threadIdx.x] = (ja >= 0 && ja < naz) || wrap;
+  }
+  __syncthreads();
+  // Core points: thread -> (row, elevation) advanced incrementally (no divisions); neighbour tests on
+  // the IEEE bits (f is floored, so positive and never NaN: the bits order like the values).  Raster
+  // order decides strictness: the row above precedes the point (strict) unless it is the wrapped
+  // last row, the row below follows it (non-strict) unless it is the wrapped first row; within the
+  // row the left neighbour precedes, the right one follows.  With naz == 1 the wrapped rows are the
+  // point's own row, whose tests repeat the in-row ones, so they are skipped.
+  const int nelI = (int)nel;
+  const long long* fi = reinterpret_cast<const long long*>(ft);
+  const bool up_ok = rowok[0] && naz > 1, dn_ok = rowok[1] && naz > 1;
+  const int steps_r = (int)(blockDim.x / nelI), steps_e = (int)(blockDim.x - steps_r * nelI);
+  int r = 1 + (int)(threadIdx.x / nelI), ie = (int)(threadIdx.x - (threadIdx.x / nelI) * nelI);
+  for (; r <= nr; r += steps_r, ie += steps_e) {
+    if (ie >= nelI) { ie -= nelI; ++r; if (r > nr) break; }
+    const int64_t ia = ia0 + r - 1;
+    const int c = r * nelI + ie;
+    const long long fp = fi[c];
+    const bool lft = ie > 0, rgt = ie < nelI - 1;
+    // same row: left strict, right non-strict
+    bool peak = (!lft || fp < fi[c - 1]) && (!rgt || fp <= fi[c + 1]);
+    const bool up = (r > 1) || up_ok, dn = (r < nr) || dn_ok;
+    if (up) {                                            // row ia - 1 (wrapped: the last row, after p)
+      const bool st = ia > 0;
+      const int u = c - nelI;
+      const long long a = fi[u], l = lft ? fi[u - 1] : 0, g = rgt ? fi[u + 1] : 0;
+      peak = peak && (st ? fp < a : fp <= a) && (!lft || (st ? fp < l : fp <= l)) && (!rgt || (st ? fp < g : fp <= g));
+    }
+    if (dn) {                                            // row ia + 1 (wrapped: the first row, before p)
+      const bool st = ia == naz - 1;
+      const int d = c + nelI;
+      const long long a = fi[d], l = lft ? fi[d - 1] : 0, g = rgt ? fi[d + 1] : 0;
+      peak = peak && (st ? fp < a : fp <= a) && (!lft || (st ? fp < l : fp <= l)) && (!rgt || (st ? fp < g : fp <= g));
+    }
+    const int64_t pidx = ia * nel + ie;
+    if (P) P[(size_t)b * L + pidx] = to_p32a(__longlong_as_double(fp));
+    if (peak) {
+      const int slot = atomicAdd(cnt + b, 1);
+      if (slot < cap) {
+        cidx[(size_t)b * cap + slot] = (int32_t)pidx;
+        cf[(size_t)b * cap + slot] = __longlong_as_double(fp);
+      }
+    }
+  }
+}
+
 template <int M>
 cudaError_t launch_scan_array_t(const doa_plan_s* p, int64_t B, cudaStream_t s) {
   using Sh = ArrShape<M>;
@@ -267,10 +346,19 @@ cudaError_t launch_array_spectrum(const doa_plan_s* p, const double* lam, const 
     default: return cudaErrorInvalidValue;
   }
   if (e != cudaSuccess) return e;
+  count_launch();
+  if (p->nel <= kPk2MaxNel && B < 65536) {
+    const int TA = (int)(kPk2Vals / p->nel < 1 ? 1 : kPk2Vals / p->nel);
+    const size_t smem = (size_t)(TA + 2) * p->nel * sizeof(double);
+    kernel_occupancy(peaks2d_tile_kernel, 256, smem);                  // sets the smem attribute (> 48 KB)
+    const dim3 grid((unsigned)((p->naz + TA - 1) / TA), (unsigned)B);
+    peaks2d_tile_kernel<<<grid, 256, smem, s>>>(p->fbuf, p->naz, p->nel, TA, p->wrap, p->cap, p->cnt, p->cand_idx,
+                                                p->cand_f, P);
+    return cudaGetLastError();
+  }
   const int64_t tot = B * p->L;
   int blocks = (int)((tot + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  count_launch();
   peaks2d_kernel<<<blocks, 256, 0, s>>>(p->fbuf, B, p->naz, p->nel, p->wrap, p->cap, p->cnt, p->cand_idx,
                                         p->cand_f, P);
   return cudaGetLastError();
