@@ -83,50 +83,37 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {   // conj(a) * 
 //         (P_n e1)_p = sum_{j<K} V[p][j] conj(V[0][j])     (Q5; e1^H P_n e1 <= 100 eps: unnormalised, G1)
 // Executed by a 16-lane group (hl = lane within it); every sum runs in a fixed ascending order, so
 // eig16h and eig16s (same eigenpairs, same routine) give bitwise identical coefficients.
-// Shared memory: two [N][N+1] double2 buffers (the eigensolver's A double buffer, so the fused
-// kernel needs no extra smem and keeps its occupancy):
-//   Vs  columns j < N: eigenvectors in rank order, Vs[p (N+1) + j] = V[p][j] (written by the caller);
-//       column N: scratch for MN's w
-//   Gs  columns j < N: scratch g_{k,j}; column N: .x = ascending eigenvalues lambda_r at row r
-//       (written by the caller), .y = EV weights
+// Shared memory (the eigensolver's own buffers, so the fused kernel needs no extra smem and keeps
+// its occupancy):
+//   Vs  [N][N+1]: columns j < N eigenvectors in rank order, Vs[p (N+1) + j] = V[p][j] (written by
+//       the caller); column N: scratch for MN's w
+//   Gs  [N][N+1] scratch g_{k,j} in columns j < N; may alias Vs (every read of Vs's columns j < N
+//       precedes the first write of Gs)
+//   LE  [N]: .x = ascending eigenvalues lambda_r (written by the caller), .y = EV weights
 // Outputs per plan a: coefficients in the scan's A-fragment layout (coef_index), cnt[b] = 0 and
 // info[b] = eigflag | DEGENERATE (overwritten).  `live`: this group holds a real frame b < B.
 template <int N>
-__device__ __forceinline__ void frame_coef(int hl, unsigned gmask, double2* Vs, double2* Gs, int M, int D,
-                                           const CoefPlans& cp, int64_t b, bool live, int eigflag) {
+__device__ __forceinline__ void frame_coef(int hl, unsigned gmask, double2* Vs, double2* Gs, double2* LE, int M,
+                                           int D, const CoefPlans& cp, int64_t b, bool live, int eigflag) {
   constexpr int LDV = N + 1;
-  auto lam = [&](int r) { return Gs[r * LDV + N].x; };
+  auto lam = [&](int r) { return LE[r].x; };
   const int K = M - D;
   bool need_ev = false, need_mn = false;
 #pragma unroll
   for (int a = 0; a < kMaxCoefPlans; ++a)
     if (a < cp.nplans) { need_ev |= cp.alg[a] == DOA_ALG_EV; need_mn |= cp.alg[a] == DOA_ALG_MN; }
-  // (a) lane j: g_{k,j} for every lag k from column j (zero beyond M)
-  {
-    const int j = hl;
-    double2 col[N];
+  // (a) lane j: column j into registers (zero beyond M)
+  const int j = hl;
+  double2 col[N];
 #pragma unroll
-    for (int p = 0; p < N; ++p) col[p] = (j < M && p < M) ? Vs[p * LDV + j] : make_double2(0.0, 0.0);
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      double gr = 0.0, gi = 0.0;
-#pragma unroll
-      for (int p = 0; p + k < N; ++p) {                 // V[p][j] conj(V[p+k][j]), ascending p
-        gr = fma(col[p].x, col[p + k].x, gr);
-        gr = fma(col[p].y, col[p + k].y, gr);
-        gi = fma(col[p].y, col[p + k].x, gi);
-        gi = fma(-col[p].x, col[p + k].y, gi);
-      }
-      if (j < N) Gs[k * LDV + j] = make_double2(gr, gi);
-    }
-  }
+  for (int p = 0; p < N; ++p) col[p] = (j < M && p < M) ? Vs[p * LDV + j] : make_double2(0.0, 0.0);
   int flag_ev = 0, flag_mn = 0;
   if (need_ev) {                                        // EV weights, lane-parallel (G1 clamp)
     const double lfloor = 100.0 * DBL_EPSILON * fmax(lam(M - 1), 0.0);
     const double lj = hl < K ? lam(hl) : 1.0;
     const bool deg = hl < K && lj <= lfloor;
     if (__ballot_sync(0xffffffffu, deg) & gmask) flag_ev = DOA_INFO_DEGENERATE;
-    if (hl < N) Gs[hl * LDV + N].y = hl < K ? (deg ? (lfloor > 0.0 ? 1.0 / lfloor : 1.0) : 1.0 / lj) : 0.0;
+    if (hl < N) LE[hl].y = hl < K ? (deg ? (lfloor > 0.0 ? 1.0 / lfloor : 1.0) : 1.0 / lj) : 0.0;
   }
   if (need_mn) {                                        // w_p on lane p, p0 on every lane (same order)
     const int p = hl;
@@ -148,6 +135,20 @@ __device__ __forceinline__ void frame_coef(int hl, unsigned gmask, double2* Vs, 
     const double lp = degen ? 1.0 : 1.0 / p0;
     if (p < N) Vs[p * LDV + N] = degen ? make_double2(wr, wi) : make_double2(wr * lp, wi * lp);   // zero for p >= M
   }
+  __syncwarp();                                         // every read of Vs's columns j < N is done
+  // g_{k,j} for every lag k from the column in registers (Gs may overwrite Vs from here on)
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double gr = 0.0, gi = 0.0;
+#pragma unroll
+    for (int p = 0; p + k < N; ++p) {                   // V[p][j] conj(V[p+k][j]), ascending p
+      gr = fma(col[p].x, col[p + k].x, gr);
+      gr = fma(col[p].y, col[p + k].y, gr);
+      gi = fma(col[p].y, col[p + k].x, gi);
+      gi = fma(-col[p].x, col[p + k].y, gi);
+    }
+    if (j < N) Gs[k * LDV + j] = make_double2(gr, gi);
+  }
   __syncwarp();
   // (b) lane k: combine over j (ascending) and write every plan's coefficients
   const int k = hl;
@@ -161,7 +162,7 @@ __device__ __forceinline__ void frame_coef(int hl, unsigned gmask, double2* Vs, 
         mus.x += g.x;
         mus.y += g.y;
         if (need_ev) {
-          const double w = Gs[j * LDV + N].y;
+          const double w = LE[j].y;
           ev.x = fma(w, g.x, ev.x);
           ev.y = fma(w, g.y, ev.y);
         }
@@ -289,17 +290,23 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
                                                                              double2* __restrict__ V_out,
                                                                              int32_t* __restrict__ info,
                                                                              int D, CoefPlans cp) {
-  __shared__ double2 As[kHWarps][2][2][N * HLd<N>::LD];          // [warp][half][buffer]
-  // rotation parameters (c, s) and (Re e, Im e) per slot pair, 16-byte entries: the pairs of a half
-  // sit in distinct bank groups, so every lane -> pair pattern is conflict-free
-  __shared__ double2 pcs[kHWarps][2][N / 2], pee[kHWarps][2][N / 2];
+  // A double buffer per half: the packed layout (off-diagonal slots < 130, diagonal doubles from
+  // slot kDiag16) for N = 16, the XOR layout for N = 8.  The frame epilogue uses the two buffers of
+  // a half as one [N][N+1] scratch (V rank-ordered, then the lag sums over it).
+  constexpr int BUF = N == 16 ? kDiag16 + 8 : N * HLd<N>::LD;
+  __shared__ double2 As[kHWarps][2][2][BUF];                       // [warp][half][buffer]
+  // rotation parameters (c, s) at [0, N/2) and (Re e, Im e) at [N/2, N) per slot pair, 16-byte
+  // entries: the pairs of a half sit in distinct bank groups, so every lane -> pair pattern is
+  // conflict-free; after the sweeps, the frame epilogue's eigenvalues / EV weights
+  __shared__ double2 prm[kHWarps][2][N];
   __shared__ int rank_s[kHWarps][2][N];
+  static_assert(2 * BUF >= N * (N + 1), "frame epilogue scratch");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int hm = lane >> 4, hl = lane & 15;
   const int64_t b = ((int64_t)blockIdx.x * kHWarps + warp) * 2 + hm;
   const bool valid = b < B;
-  double2* const Pc = pcs[warp][hm];
-  double2* const Pe = pee[warp][hm];
+  double2* const Pc = prm[warp][hm];
+  double2* const Pe = prm[warp][hm] + N / 2;
 
   // ||R||_F and off(A) are summed in the same order as eig16s's (lane partials over the element
   // strides of 32, i.e. this half-lane's even and odd strides of 16, added, then the tree), so both
@@ -461,9 +468,7 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
     }
     rank_s[warp][hm][hl] = rk;
     if (valid && lam_out) lam_out[(size_t)b * M + rk] = li;
-    // column N of frame_coef's [N][N+1] view of this buffer: off-diagonal slots no longer needed
-    // (N = 16) or never used (N = 8), and never the diagonal being read here (slots kDiag16..+7)
-    if (FUSE) A[rk * (N + 1) + N].x = li;
+    if (FUSE) prm[warp][hm][rk].x = li;               // the rotation parameters are no longer needed
   }
   __syncwarp();
   if (valid && hl < M && V_out) {
@@ -474,16 +479,16 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
   }
   if (valid && hl == 0 && info) info[b] = flag;
   if (FUSE) {
-    // rank-ordered V into the free buffer, then S3 with the A buffer as scratch (its diagonal has
-    // been read by every lane before the __syncwarp above)
-    double2* Vs = As[warp][hm][cur ^ 1];
+    // rank-ordered V over both buffers (every lane has read A's diagonal before the __syncwarp
+    // above), then S3 with the lag sums overwriting it in place
+    double2* Vs = &As[warp][hm][0][0];
     if (hl < M) {
 #pragma unroll
       for (int k = 0; k < N; ++k)
         if (k < M) Vs[hl * (N + 1) + rank_s[warp][hm][k]] = v[k];
     }
     __syncwarp();
-    frame_coef<N>(hl, hm ? 0xffff0000u : 0x0000ffffu, Vs, A, M, D, cp, b, valid, flag);
+    frame_coef<N>(hl, hm ? 0xffff0000u : 0x0000ffffu, Vs, Vs, prm[warp][hm], M, D, cp, b, valid, flag);
   }
 }
 
@@ -762,7 +767,7 @@ __global__ void __launch_bounds__(kSThreads) eig16s_kernel(const double2* __rest
     }
     rank_s[lane] = rk;
     if (lam_out) lam_out[(size_t)b * M + rk] = li;
-    if (FUSE) As[1][rk * (N + 1) + N].x = li;           // column N: never used by A
+    if (FUSE) (&Pcs[0][0])[rk].x = li;                  // the rotation parameters are no longer needed
   }
   __syncthreads();
   if (warp == 1 && vrow < M) {
@@ -785,7 +790,8 @@ __global__ void __launch_bounds__(kSThreads) eig16s_kernel(const double2* __rest
     if (warp == 0) flag = __shfl_sync(0xffffffffu, flag, 0);
     __syncthreads();
     if (warp == 0)
-      frame_coef<N>(lane & 15, lane < 16 ? 0x0000ffffu : 0xffff0000u, As[0], As[1], M, D, cp, b, lane < 16, flag);
+      frame_coef<N>(lane & 15, lane < 16 ? 0x0000ffffu : 0xffff0000u, As[0], As[1], &Pcs[0][0], M, D, cp, b,
+                    lane < 16, flag);
   }
 }
 
