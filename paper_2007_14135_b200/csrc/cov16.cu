@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(kSplitMax * 32) cov16_multi_kernel(const float
     acc[t][1] = tot[t * 64 + 2 * lane + 1];
   }
   if (lane == 0) ticket[b] = 0u;                          // ready for the next call
+  __syncwarp();                                           // tot (red[1..]) is read before G overwrites it
   gram_to_r(acc, &red[0][0][0], lane, N, M, R + (size_t)b * M * M);
 }
 

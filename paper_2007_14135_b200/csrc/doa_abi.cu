@@ -274,6 +274,9 @@ doa_status_t doa_plan_create(doa_plan_t* plan, int32_t M, double d_over_lambda, 
   al((void**)&p->cand_idx, B * cap * sizeof(int32_t));
   al((void**)&p->cand_f, B * cap * sizeof(double));
   al((void**)&p->coef, doa::coef_words(max_batch, M) * sizeof(double));
+  // the DMMA scan reads whole 8-frame groups: rows of frames past B in the last group must hold
+  // defined values (their results are discarded)
+  if (e == cudaSuccess) e = cudaMemset(p->coef, 0, doa::coef_words(max_batch, M) * sizeof(double));
   if (e != cudaSuccess) {
     doa_plan_destroy(p);
     return cuda_fail(e, "doa_plan_create: workspace allocation");
@@ -324,6 +327,7 @@ doa_status_t doa_plan_create_array(doa_plan_t* plan, int32_t M, const double* po
   al((void**)&p->cand_idx, B * p->cap * sizeof(int32_t));
   al((void**)&p->cand_f, B * p->cap * sizeof(double));
   al((void**)&p->coef, kw * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemset(p->coef, 0, kw * sizeof(double));   // partial last 8-frame group
   al((void**)&p->dpos, dp.size() * sizeof(double));
   al((void**)&p->fbuf, B * (size_t)L * sizeof(double));
   if (e == cudaSuccess) e = cudaMemcpy(p->dpos, dp.data(), dp.size() * sizeof(double), cudaMemcpyHostToDevice);
