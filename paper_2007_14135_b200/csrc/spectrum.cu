@@ -40,12 +40,6 @@ __device__ __forceinline__ void bar_arrive(int id) {
   if (id == 1) asm volatile("bar.arrive 1, 256;\n" ::: "memory");
   else asm volatile("bar.arrive 2, 256;\n" ::: "memory");
 }
-#ifdef DOA_SCAN_PAIR_PP
-// A/B variant (no gain measured): warps w and w+4 (same SM sub-partition) hand the DMMA pipe back
-// and forth on their own barriers 1 + 2(w%4) and 2 + 2(w%4) (64 threads), decoupled from the others.
-__device__ __forceinline__ void pbar_sync(int id) { asm volatile("bar.sync %0, 64;\n" :: "r"(id) : "memory"); }
-__device__ __forceinline__ void pbar_arrive(int id) { asm volatile("bar.arrive %0, 64;\n" :: "r"(id) : "memory"); }
-#endif
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -573,12 +567,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
   const int64_t nit = (g1 - g0 + kCtaWarps - 1) / kCtaWarps;
   PendingCand pcand;
   pcand.slot = -1; pcand.b = 0; pcand.idx = 0; pcand.f = 0;
-#ifdef DOA_SCAN_PAIR_PP
-  const int pbase = 1 + 2 * (warp & 3);
-  if (wg == 1) pbar_arrive(pbase);
-#else
   if (wg == 1) bar_arrive(1);
-#endif
   for (int64_t it = 0; it < nit; ++it) {
     const int64_t g = g0 + warp + it * kCtaWarps;
     const bool gv = g < g1;                                      // warp-uniform
@@ -607,11 +596,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
 #pragma unroll
         for (int t = 0; t < (MIRROR ? NA : 1); ++t) { aco[t][0] = 0.0; aco[t][1] = 0.0; }
       }
-#ifdef DOA_SCAN_PAIR_PP
-      pbar_sync(pbase + wg);
-#else
       bar_sync(1 + wg);                         // my group's turn on the pipe
-#endif
       if (gv) {
         if (!MIRROR) {
 #pragma unroll
@@ -640,11 +625,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
           }
         }
       }
-#ifdef DOA_SCAN_PAIR_PP
-      pbar_arrive(pbase + 1 - wg);
-#else
       bar_arrive(2 - wg);                       // hand the pipe to the other group
-#endif
       if (!gv) continue;
       flush_cand(pcand, cap, cidx, cf);                // the previous epilogue's deferred candidate
       if (!MIRROR) {
@@ -671,11 +652,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
     }
   }
   flush_cand(pcand, cap, cidx, cf);
-#ifdef DOA_SCAN_PAIR_PP
-  if (wg == 0) pbar_sync(pbase);
-#else
   if (wg == 0) bar_sync(1);                       // consume the other group's last hand-off
-#endif
 }
 
 template <int S, bool MIRROR>
