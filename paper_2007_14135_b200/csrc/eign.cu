@@ -193,17 +193,19 @@ __global__ void __launch_bounds__(EigN<N>::T, 1) eigN_kernel(const double2* __re
         // r = |a_xy|, h = sqrt(d^2 + r^2), q = |d| + h:  t = sign(d) r / q,  c = sqrt(q / 2h),
         // s = sign(d) r / sqrt(2 h q)  (c^2 + s^2 = 1 exactly in exact arithmetic), t r = sign(d) r^2 / q.
         // c's critical path is two MUFU+Newton reciprocal square roots instead of four chained
-        // reciprocal (square) roots; s, e and t r run on parallel branches.
-        const double ir = rsqrt_p(rot ? r2 : 1.0);          // 1/|a_xy|
+        // reciprocal (square) roots; s, e and t r run on parallel branches.  The MUFU inputs are not
+        // guarded (a zero pivot gives inf/NaN intermediates): the identity is selected at the end,
+        // keeping selects off the chain.
+        const double ir = rsqrt_p(r2);          // 1/|a_xy|
         const double rr = r2 * ir;                            // |a_xy|
         const double d = 0.5 * (ayy - axx);
         const double h2 = fma(d, d, r2);
-        const double irh = rsqrt_p(rot ? h2 : 1.0);          // 1/h
+        const double irh = rsqrt_p(h2);          // 1/h
         const double h = h2 * irh;
         const double q = fabs(d) + h;
         const double u = 0.5 * q * irh;                       // c^2, in [1/2, 1]
         const double sabs = rr * rsqrt_p(2.0 * h * q);
-        const double trabs = r2 * rcp_p(rot ? q : 1.0);
+        const double trabs = r2 * rcp_p(q);
         const double tr = rot ? (d < 0.0 ? -trabs : trabs) : 0.0;   // t |a_xy|
         PrmN p;
         p.c = rot ? u * rsqrt_p(u) : 1.0;
