@@ -49,7 +49,7 @@ def parse():
                          "weak: every GPU owns a full batch")
     ap.add_argument("--no-north-star", dest="north_star", action="store_false",
                     help="skip the north-star (ns) measurement that the default c4 run adds")
-    ap.add_argument("--engine", default="toeplitz_fp64", choices=["toeplitz_fp64", "direct_fp32"],
+    ap.add_argument("--engine", default="toeplitz_fp64", choices=["toeplitz_fp64", "direct_fp32", "direct_tf32x3"],
                     help="scan engine of the ULA plans (doa_plan_set_engine): the product's fp64 Toeplitz DMMA "
                          "contraction, or the NEXT-2 FP32-pipe direct form (A/B evidence)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle CPU time for cpu_baseline")
@@ -337,6 +337,14 @@ def scan_roofline(wl, is_array, mirrored):
     spec_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in wl.spec_ev)
     if not is_array:                               # doa_scan_multi: the four plans' launches back to back
         spec_ms /= len(ALGS)
+    if wl.engine == "direct_tf32x3":               # tcgen05 GEMM: 3 tf32 products of (128 angles x 256 cols x K 32)
+        # algorithmic work of the direct form (as for the FP32-pipe engine); peak = dense tf32 (MEASURED_PEAKS
+        # bf16 x the guide's tf32:bf16 ratio 1/2)
+        nv = [(M - cfg.D) if a in ("music", "ev") else 1 for a in ALGS]
+        scan_flops = sum(n * (8.0 * M + 4.0) for n in nv) / len(nv) * L * B
+        pk = peaks_json()
+        tf32_peak = float(pk.get("bf16_tflops", pk.get("cublas_bf16_tflops", 2250.0))) / 2.0
+        return spec_ms, scan_flops, scan_flops / (spec_ms / 1e3) / 1e12, tf32_peak
     if wl.engine == "direct_fp32":                 # per vector x_j: 4M FFMA for x_j^H a, 2 for |.|^2; mean over plans
         nv = [(M - cfg.D) if a in ("music", "ev") else 1 for a in ALGS]
         scan_flops = sum(n * (8.0 * M + 4.0) for n in nv) / len(nv) * L * B
@@ -469,6 +477,11 @@ def main():
                 "share_of_step": spec_ms * len(ALGS) / ms_step,
                 "peak_source": "148 SMs x 64 FP64 lanes x 2 flop x sm_max_mhz (guide unit counts; "
                                "measured DMMA 37.18 / DFMA 34.19 TFLOP/s in profiles/fp64_peaks_r01.txt)"}
+    if wl.engine == "direct_tf32x3":
+        roofline.update({"bound": "tensor", "kernel": "scan_tc_kernel (NEXT-2 direct form on tcgen05 kind::tf32, 3xTF32, "
+                                   "TMEM accumulators), one launch per estimator, timed via doa_scan_multi",
+                         "algorithmic_flops_per_point": scan_flops / (L * B),
+                         "peak_source": "MEASURED_PEAKS.json bf16 dense x 1/2 (tf32:bf16 ratio of the guide)"})
     if wl.engine == "direct_fp32":
         roofline.update({"kernel": "scan_f32_kernel (NEXT-2 FP32-pipe direct form), one launch per estimator, "
                                    "timed via doa_scan_multi (mean per launch)",

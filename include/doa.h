@@ -122,7 +122,10 @@ doa_status_t doa_plan_info(doa_plan_t plan, doa_plan_info_t* out);
  *   DOA_ENGINE_DIRECT_FP32: the paper's own direct form f = sum_j |x_j^H a|^2 over the weighted
  *     noise vectors x_j = sqrt(w_j) e_j (MN: the normalised w; PHD: e_min), one thread per angle
  *     as in §4.3, every product and sum on the FP32 pipe (vectors and steering formed in
- *     fp64 and rounded to fp32; north_star's "FP32-pipe sincos+FMA" alternative).  It is an A/B
+ *     fp64 and rounded to fp32; north_star's "FP32-pipe sincos+FMA" alternative);
+ *   DOA_ENGINE_DIRECT_TF32X3: the same direct form as a GEMM on the 5th-generation tensor cores
+ *     (tcgen05.mma kind::tf32 with TMEM accumulators; every fp32 operand split into tf32 head and
+ *     tail, three products: ~fp32 accuracy).  Both direct-form engines are A/B
  *     engine for evidence: several times slower than the Toeplitz contraction at c4, and its fp32
  *     rounding can move peak indices and exceed 1e-3 dB near deep nulls
  *     (tests/test_gpu_fp32_engine.py).
@@ -130,9 +133,9 @@ doa_status_t doa_plan_info(doa_plan_t plan, doa_plan_info_t* out);
  * engine (doa_run_multi keeps the eigendecomposition shared; the frame kernel is used only when
  * every plan is Toeplitz).  The fp32 engine allocates max_batch*(M-D)*M complex64 (synchronous).
  * Errors: NULL plan or unknown engine -> DOA_ERR_INVALID_ARG; general-array plans, or
- * DOA_ENGINE_DIRECT_FP32 with M > 16 -> DOA_ERR_UNSUPPORTED; allocation failure ->
+ * a direct-form engine with M > 16 -> DOA_ERR_UNSUPPORTED; allocation failure ->
  * DOA_ERR_OUT_OF_MEMORY.  Must not be called while work on the plan is in flight. */
-enum { DOA_ENGINE_TOEPLITZ_FP64 = 0, DOA_ENGINE_DIRECT_FP32 = 1 };
+enum { DOA_ENGINE_TOEPLITZ_FP64 = 0, DOA_ENGINE_DIRECT_FP32 = 1, DOA_ENGINE_DIRECT_TF32X3 = 2 };
 doa_status_t doa_plan_set_engine(doa_plan_t plan, int32_t engine);
 
 /* S1 — sample covariance, Eq. 3 / Table 2 Step-1:

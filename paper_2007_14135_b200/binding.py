@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DOA_LIB") or os.path.join(_HERE, "libdoa.so")   # DOA_LIB: tuning builds only
 
 ALG = {"phd": 0, "music": 1, "ev": 2, "mn": 3}
-ENGINE = {"toeplitz_fp64": 0, "direct_fp32": 1}           # doa_plan_set_engine (include/doa.h)
+ENGINE = {"toeplitz_fp64": 0, "direct_fp32": 1, "direct_tf32x3": 2}           # doa_plan_set_engine (include/doa.h)
 INFO_NOCONV, INFO_DEGENERATE, INFO_CAND_OVERFLOW, INFO_UNDERDETERMINED = 1, 2, 4, 8
 STATUS = {0: "DOA_OK", 1: "DOA_ERR_INVALID_ARG", 2: "DOA_ERR_UNSUPPORTED", 3: "DOA_ERR_OUT_OF_MEMORY",
           4: "DOA_ERR_CUDA"}
@@ -350,7 +350,8 @@ class Plan:
             self.set_engine(engine)
 
     def set_engine(self, engine):
-        """"toeplitz_fp64" (the product) or "direct_fp32" (SURVEY §8(f) NEXT-2 A/B engine)."""
+        """"toeplitz_fp64" (the product), "direct_fp32" or "direct_tf32x3" (SURVEY §8(f) NEXT-2 A/B engines:
+        the direct form on the FP32 pipe or on tcgen05 tensor cores)."""
         with torch.cuda.device(self.device):
             doa_plan_set_engine(self.h, engine)
         self.engine = engine

@@ -78,10 +78,10 @@ cudaError_t ensure_run_scratch(doa_plan_s* p) {
 cudaError_t spectrum_stage(const doa_plan_s* p, const double* lam, const double* V, int64_t B, float* P,
                            int32_t* info, cudaStream_t s) {
   if (p->geom == 1) return doa::launch_array_spectrum(p, lam, V, B, P, info, s);
-  if (p->engine == DOA_ENGINE_DIRECT_FP32) {
+  if (p->engine != DOA_ENGINE_TOEPLITZ_FP64) {
     cudaError_t e = doa::launch_vec32(p, lam, V, B, info, s);
     if (e != cudaSuccess) return e;
-    return doa::launch_scan_f32(p, B, P, s);
+    return doa::launch_scan_direct_form(p, B, P, s);
   }
   cudaError_t e = doa::launch_coef(p, lam, V, B, info, s);
   if (e != cudaSuccess) return e;
@@ -95,8 +95,8 @@ cudaError_t scan_stage(doa_plan_s* const* plans, int nplans, int64_t B, float* P
   cudaError_t e = cudaSuccess;
   for (int a = 0; a < nplans && e == cudaSuccess;) {
     if (plans[a]->geom == 1) { ++a; continue; }
-    if (plans[a]->engine == DOA_ENGINE_DIRECT_FP32) {
-      e = doa::launch_scan_f32(plans[a], B, nplans == 1 ? P : nullptr, st);
+    if (plans[a]->engine != DOA_ENGINE_TOEPLITZ_FP64) {
+      e = doa::launch_scan_direct_form(plans[a], B, nplans == 1 ? P : nullptr, st);
       ++a;
       continue;
     }
@@ -143,7 +143,7 @@ cudaError_t run_plans(doa_plan_s* const* plans, int nplans, const float* X, int6
     for (int a = 0; a < nplans && e == cudaSuccess; ++a) {
       doa_plan_s* q = plans[a];
       if (q->geom == 1) e = doa::launch_array_spectrum(q, p->lam, p->V, B, nplans == 1 ? P : nullptr, info + (size_t)a * ldo, st);
-      else if (q->engine == DOA_ENGINE_DIRECT_FP32) e = doa::launch_vec32(q, p->lam, p->V, B, info + (size_t)a * ldo, st);
+      else if (q->engine != DOA_ENGINE_TOEPLITZ_FP64) e = doa::launch_vec32(q, p->lam, p->V, B, info + (size_t)a * ldo, st);
       else if (nu < 64) { ula[nu] = q; ula_info[nu++] = info + (size_t)a * ldo; }
       else e = doa::launch_coef(q, p->lam, p->V, B, info + (size_t)a * ldo, st);
     }
@@ -373,11 +373,11 @@ doa_status_t doa_plan_info(doa_plan_t p, doa_plan_info_t* out) {
 doa_status_t doa_plan_set_engine(doa_plan_t p, int32_t engine) {
   g_launches = 0;
   DOA_CHECK_PLAN(p);
-  if (engine != DOA_ENGINE_TOEPLITZ_FP64 && engine != DOA_ENGINE_DIRECT_FP32)
+  if (engine != DOA_ENGINE_TOEPLITZ_FP64 && engine != DOA_ENGINE_DIRECT_FP32 && engine != DOA_ENGINE_DIRECT_TF32X3)
     return fail(DOA_ERR_INVALID_ARG, "doa_plan_set_engine: unknown engine %d", engine);
   if (p->geom != 0) return fail(DOA_ERR_UNSUPPORTED, "doa_plan_set_engine: general-array plans have one engine");
-  if (engine == DOA_ENGINE_DIRECT_FP32) {
-    if (p->M > 16) return fail(DOA_ERR_UNSUPPORTED, "doa_plan_set_engine: the fp32 engine supports M <= 16 (M=%d)", p->M);
+  if (engine != DOA_ENGINE_TOEPLITZ_FP64) {
+    if (p->M > 16) return fail(DOA_ERR_UNSUPPORTED, "doa_plan_set_engine: the direct-form engines support M <= 16 (M=%d)", p->M);
     if (!p->x32)
       DOA_TRY(cudaMalloc((void**)&p->x32, (size_t)p->max_batch * (p->M - p->D) * p->M * 2 * sizeof(float)),
               "doa_plan_set_engine: vectors");
@@ -505,8 +505,8 @@ doa_status_t doa_scan_multi(const doa_plan_t* plans, int32_t nplans, int64_t B, 
     grp[a] = plans[a];
     DOA_TRY(cudaMemsetAsync(plans[a]->cnt, 0, (size_t)B * sizeof(int32_t), st2), "doa_scan_multi: counters");
   }
-  if (plans[0]->engine == DOA_ENGINE_DIRECT_FP32) {
-    for (int a = 0; a < nplans; ++a) DOA_TRY(doa::launch_scan_f32(plans[a], B, nullptr, st2), "doa_scan_multi");
+  if (plans[0]->engine != DOA_ENGINE_TOEPLITZ_FP64) {
+    for (int a = 0; a < nplans; ++a) DOA_TRY(doa::launch_scan_direct_form(plans[a], B, nullptr, st2), "doa_scan_multi");
   } else {
     DOA_TRY(doa::launch_scan_plans(grp, nplans, B, nullptr, st2), "doa_scan_multi");
   }

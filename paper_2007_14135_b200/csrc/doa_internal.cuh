@@ -199,6 +199,13 @@ cudaError_t launch_scan_direct(const DirectScanArgs& args, const doa_plan_s* p, 
 cudaError_t launch_vec32(const doa_plan_s* p, const double* lam, const double* V, int64_t B, int32_t* info,
                          cudaStream_t s);
 cudaError_t launch_scan_f32(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s);
+// the same direct form on the 5th-generation tensor cores: tcgen05.mma kind::tf32, 3xTF32 split,
+// accumulators in TMEM (csrc/scan_tc.cu)
+cudaError_t launch_scan_tc(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s);
+// S4-S6 of a direct-form engine plan (DOA_ENGINE_DIRECT_FP32 or DOA_ENGINE_DIRECT_TF32X3)
+inline cudaError_t launch_scan_direct_form(const doa_plan_s* p, int64_t B, float* P, cudaStream_t s) {
+  return p->engine == DOA_ENGINE_DIRECT_TF32X3 ? launch_scan_tc(p, B, P, s) : launch_scan_f32(p, B, P, s);
+}
 // plans that may share one direct scan launch (same M, d/lambda, grid; ULA)
 bool direct_compatible(const doa_plan_s* a, const doa_plan_s* b);
 // general-array plans (csrc/array.cu): coefficients, scan into fbuf, 2-D candidates (+ optional P)

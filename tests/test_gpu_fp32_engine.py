@@ -1,5 +1,7 @@
-"""NEXT-2: the FP32-pipe direct-form scan engine behind the ABI
-(doa_plan_set_engine(plan, DOA_ENGINE_DIRECT_FP32); csrc/scan_fp32.cu), against the fp64 oracle.
+"""NEXT-2: the direct-form scan engines behind the ABI — on the FP32 pipe
+(doa_plan_set_engine(plan, DOA_ENGINE_DIRECT_FP32); csrc/scan_fp32.cu) and on the tcgen05 tensor
+cores (DOA_ENGINE_DIRECT_TF32X3, 3xTF32 with TMEM accumulators; csrc/scan_tc.cu) — against the
+fp64 oracle.
 
 It is the A/B alternative to the product's fp64 Toeplitz contraction, not the product: fp32
 rounding of f = sum_j |x_j^H a|^2 costs ~1e-7 relative in f, which near a deep null can reach the
@@ -38,11 +40,15 @@ def doa():
         json.dump(STATS, fh, indent=1)
 
 
-def _check(doa, cfgname, cfg, X, tag):
+ENGINES = ["direct_fp32", "direct_tf32x3"]     # FP32 pipe / tcgen05 tensor cores (3xTF32)
+
+
+def _check(doa, cfgname, cfg, X, tag, engine):
     B = X.shape[0]
+    tag = f"{engine}/{tag}"
     for alg in ALGS:
         plan = doa.Plan(cfg.M, cfg.D, alg, cfg.dtheta, L=cfg.L, theta0=cfg.theta0, max_batch=B,
-                        engine="direct_fp32")
+                        engine=engine)
         idx, val, npk, info, P = plan.run(torch.from_numpy(X).cuda(), want_P=True)
         idx, P, info = idx.cpu().numpy(), P.cpu().numpy(), info.cpu().numpy()
         worst_db, exact, total, off, swaps, overflow = 0.0, 0, 0, 0, 0, 0
@@ -82,15 +88,34 @@ def _check(doa, cfgname, cfg, X, tag):
         plan.close()
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("cfgname", ["c1", "c2", "c3_0.001"])
-def test_fp32_engine_single_frame(doa, cfgname):
+def test_fp32_engine_single_frame(doa, cfgname, engine):
     cfg = get_config(cfgname)
-    _check(doa, cfgname, cfg, generate(cfg), cfgname)
+    _check(doa, cfgname, cfg, generate(cfg), cfgname, engine)
 
 
-def test_fp32_engine_batch(doa):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_fp32_engine_batch(doa, engine):
     cfg = get_config("c4").with_(dtheta=0.05)
-    _check(doa, "c4", cfg, generate(cfg, frames=range(64)), "c4_0.05_64")
+    _check(doa, "c4", cfg, generate(cfg, frames=range(64)), "c4_0.05_64", engine)
+
+
+def test_tf32x3_engine_matches_fp32_engine(doa):
+    """The tcgen05 GEMM and the FP32-pipe loop evaluate the same direct form at ~fp32 accuracy: their
+    spectra agree to fp32-level relative error on a batch with a ragged last 8-frame chunk (M = 12)."""
+    cfg = get_config("c4").with_(M=12, D=3, dtheta=0.1)
+    B = 37
+    X = torch.from_numpy(generate(cfg, frames=range(B))).cuda()
+    for alg in ALGS:
+        Ps = []
+        for eng in ENGINES:
+            p = doa.Plan(cfg.M, cfg.D, alg, cfg.dtheta, max_batch=B, engine=eng)
+            Ps.append(p.run(X, want_P=True)[4].cpu().numpy().astype(np.float64))
+            p.close()
+        assert np.all(np.isfinite(Ps[1]))
+        assert np.max(np.abs(Ps[1] - Ps[0]) / Ps[0]) <= 3e-2, alg       # worst case near deep (MN/PHD) nulls
+        assert np.median(np.abs(Ps[1] - Ps[0]) / Ps[0]) <= 1e-5, alg
 
 
 def test_fp32_engine_plumbing(doa):
