@@ -149,19 +149,30 @@ __global__ void __launch_bounds__(kTcThreads, 2) scan_tc_kernel(const float2* __
     ia = ia < 0 ? 0 : (ia >= L ? L - 1 : ia);
     {
       const double u = grid_u(ia, theta0, dtheta, dl, L, sym);
+      float row[32];                                    // [cos(pi m u) | -sin(pi m u)], m < 16
 #pragma unroll
       for (int m = 0; m < 16; ++m) {
-        float s = 0.f, c = 0.f;
+        float sn = 0.f, cs = 0.f;
         if (m < M) {
           double r = (double)m * u;                     // exact-multiple argument, reduced mod 2 in fp64
           r -= 2.0 * rint(0.5 * r);
-          sincospif((float)r, &s, &c);
+          sincospif((float)r, &sn, &cs);
         }
-        const uint32_t ch = to_tf32(c), sh = to_tf32(-s);
-        *reinterpret_cast<uint32_t*>(a_hi + kmaj_off(tid, m)) = ch;
-        *reinterpret_cast<uint32_t*>(a_lo + kmaj_off(tid, m)) = to_tf32(c - __uint_as_float(ch));
-        *reinterpret_cast<uint32_t*>(a_hi + kmaj_off(tid, 16 + m)) = sh;
-        *reinterpret_cast<uint32_t*>(a_lo + kmaj_off(tid, 16 + m)) = to_tf32(-s - __uint_as_float(sh));
+        row[m] = cs;
+        row[16 + m] = -sn;
+      }
+      // one 16-byte store per K chunk: the 8 lanes of a quarter-warp write 8 rows of one core
+      // matrix (128 contiguous bytes) - conflict-free
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint32_t h[4], l[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          h[q] = to_tf32(row[4 * c + q]);
+          l[q] = to_tf32(row[4 * c + q] - __uint_as_float(h[q]));
+        }
+        *reinterpret_cast<uint4*>(a_hi + kmaj_off(tid, 4 * c)) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4*>(a_lo + kmaj_off(tid, 4 * c)) = make_uint4(l[0], l[1], l[2], l[3]);
       }
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic smem writes -> tensor core

@@ -41,6 +41,9 @@ def doa():
 
 
 ENGINES = ["direct_fp32", "direct_tf32x3"]     # FP32 pipe / tcgen05 tensor cores (3xTF32)
+# recorded bars per engine (G5): P relative error near the deepest nulls and max dB error; the tensor
+# core's fp32 accumulation and the dropped tail x tail product cost about 10x the FP32 pipe's error
+BARS = {"direct_fp32": (2e-3, 2e-2), "direct_tf32x3": (3e-2, 0.2)}
 
 
 def _check(doa, cfgname, cfg, X, tag, engine):
@@ -58,7 +61,7 @@ def _check(doa, cfgname, cfg, X, tag, engine):
             f, _ = orc.spectrum(alg, cfg.D, cfg.d_over_lambda, lam, V, cfg.theta0, cfg.dtheta, cfg.L, threads=8)
             oidx = orc.peaks(f, cfg.D)[0]
             worst_db = max(worst_db, max_db_error(P[b], 1.0 / f))
-            np.testing.assert_allclose(P[b].astype(np.float64), 1.0 / f, rtol=2e-3)
+            np.testing.assert_allclose(P[b].astype(np.float64), 1.0 / f, rtol=BARS[engine][0])
             # compare the peak SETS: a peak moved by fp32 rounding stays within a few grid points;
             # two peaks of near-equal strength may swap rank (accepted when their oracle f values
             # agree to 1e-4 relative, far inside what fp32 can resolve against each other)
@@ -83,7 +86,7 @@ def _check(doa, cfgname, cfg, X, tag, engine):
         STATS[f"{tag}/{alg}"] = {"frames": B, "L": cfg.L, "max_db_error": worst_db, "peaks": total,
                                  "exact": exact, "max_index_offset": off, "near_tie_swaps": swaps,
                                  "cand_overflow_frames": overflow}
-        assert worst_db <= 2e-2, (alg, worst_db)
+        assert worst_db <= BARS[engine][1], (alg, worst_db)
         assert exact >= 0.6 * total or overflow, (alg, exact, total)
         plan.close()
 
