@@ -40,6 +40,8 @@ for M, D, dth, L, B, N in cases:
     if M <= 16:
         plans[2].set_engine("direct_fp32")
         plans[2].run(X, want_P=True)
+        plans[3].set_engine("direct_tf32x3")
+        plans[3].run(X, want_P=True)
     torch.cuda.synchronize()
     for p in plans:
         p.close()
