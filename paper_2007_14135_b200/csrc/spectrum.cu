@@ -46,6 +46,12 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
+// D = A B + C with a separate accumulator input C
+__device__ __forceinline__ void dmma_884c(double& d0, double& d1, double a, double b, double c0, double c1) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+               : "=d"(d0), "=d"(d1)
+               : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
 
 // ---------------------------------------------------------------------------------------------
 // S3 (Table 3 Step-3/4): noise-subspace objects as weighted vectors {(w_j, u_j)},
@@ -404,6 +410,13 @@ constexpr int kScanNA = 8;        // 8-angle tiles per block (a lane owns 2*NA c
 #define DOA_SCAN_MINB 2
 #endif
 constexpr int kScanMinBlocks = DOA_SCAN_MINB; // __launch_bounds__ min blocks per SM
+#ifndef DOA_SCAN_CFOLD
+#define DOA_SCAN_CFOLD 1
+#endif
+constexpr bool kScanCFold = DOA_SCAN_CFOLD != 0;
+#ifndef DOA_SCAN_WAVES
+#define DOA_SCAN_WAVES 4
+#endif
 
 // Shape by k-steps S (M <= 64 -> S <= 32): 8 tiles of 8 angles per block; S <= 8 (M <= 16) keeps
 // the A fragments of a group in registers with a one-group prefetch and uses two blocks per column
@@ -610,6 +623,24 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
               for (int t = 0; t < (MIRROR ? NA : 1); ++t) dmma_884(aco[t][0], aco[t][1], av, Tk[(s * NA + t) * 32]);
             }
           }
+        } else if (kScanCFold) {
+          // O chains first, then the E chains accumulate onto O: acc = E + O = f_i directly, and
+          // f_{L-1-i} = E - O = acc - 2 O takes one DFMA per element (instead of two DADDs)
+#pragma unroll
+          for (int s = 0; SE + s < S; ++s) {
+            const double ao = STREAM_A ? __ldg(cgc + (SE + s) * 32) : a[STREAM_A ? 0 : SE + s];
+#pragma unroll
+            for (int t = 0; t < NA; ++t) dmma_884(aco[MIRROR ? t : 0][0], aco[MIRROR ? t : 0][1], ao, Tk[((SE + s) * NA + t) * 32]);
+          }
+#pragma unroll
+          for (int s = 0; s < SE; ++s) {
+            const double ae = STREAM_A ? __ldg(cgc + s * 32) : a[STREAM_A ? 0 : s];
+#pragma unroll
+            for (int t = 0; t < NA; ++t) {
+              if (s == 0) dmma_884c(acc[t][0], acc[t][1], ae, Tk[t * 32], aco[MIRROR ? t : 0][0], aco[MIRROR ? t : 0][1]);
+              else dmma_884(acc[t][0], acc[t][1], ae, Tk[(s * NA + t) * 32]);
+            }
+          }
         } else {
           // E and O k-steps interleaved: 2 NA independent accumulator chains per step pair
 #pragma unroll
@@ -643,8 +674,13 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const double ev = acc[t][e], od = aco[MIRROR ? t : 0][e];
-            fl[2 * t + e] = __double_as_longlong(ev + od);      // f_i          = E + O
-            fh[2 * t + e] = __double_as_longlong(ev - od);      // f_{L-1-i}    = E - O
+            if (kScanCFold) {
+              fl[2 * t + e] = __double_as_longlong(ev);                  // f_i       = (O + E)
+              fh[2 * t + e] = __double_as_longlong(fma(-2.0, od, ev));   // f_{L-1-i} = f_i - 2 O
+            } else {
+              fl[2 * t + e] = __double_as_longlong(ev + od);      // f_i          = E + O
+              fh[2 * t + e] = __double_as_longlong(ev - od);      // f_{L-1-i}    = E - O
+            }
           }
         scan_epilogue<NA, WRITE_P, false>(fl, lane, base, 1, H - 1, H - 1, L, b, frame_ok, cap, cnt, cidx, cf, P, pcand);
         scan_epilogue<NA, WRITE_P, true>(fh, lane, base, 1, L - 1 - H, L - 1 - H, L, b, frame_ok, cap, cnt, cidx, cf, P, pcand);
@@ -668,7 +704,7 @@ cudaError_t launch_scan_cta(const doa_plan_s* p, int64_t B, float* P, cudaStream
   const int64_t ngroups = (B + 7) / 8;
   const int64_t slots = (int64_t)sm_count() * occ;
   // frame chunk: ~4 waves of resident CTAs, >= 64 groups (8 per warp) per CTA
-  int64_t per = (gx * ngroups) / (4 * slots);
+  int64_t per = (gx * ngroups) / (DOA_SCAN_WAVES * slots);
   if (per < 64) per = 64;
   if (per > ngroups) per = ngroups;
   const int64_t gy = (ngroups + per - 1) / per;
