@@ -414,6 +414,14 @@ constexpr int kScanMinBlocks = DOA_SCAN_MINB; // __launch_bounds__ min blocks pe
 #define DOA_SCAN_CFOLD 1
 #endif
 constexpr bool kScanCFold = DOA_SCAN_CFOLD != 0;
+#ifndef DOA_SCAN_NOPF
+#define DOA_SCAN_NOPF 1
+#endif
+constexpr bool kScanNoPrefetch = DOA_SCAN_NOPF != 0;
+#ifndef DOA_SCAN_HANDOFF
+#define DOA_SCAN_HANDOFF -1
+#endif
+constexpr int kScanHandoff = DOA_SCAN_HANDOFF;   // E k-step at which the pipe is handed over (-1: end)
 #ifndef DOA_SCAN_WAVES
 #define DOA_SCAN_WAVES 4
 #endif
@@ -566,7 +574,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
   const int64_t g0 = y * per;
   const int64_t g1 = (g0 + per < ngroups) ? g0 + per : ngroups;
   double an[SA];
-  if (!STREAM_A && g0 + warp < g1) {
+  if (!kScanNoPrefetch && !STREAM_A && g0 + warp < g1) {
     const double* cg = coef + ((size_t)(g0 + warp) * S) * 32 + lane;
 #pragma unroll
     for (int s = 0; s < SA; ++s) an[s] = __ldg(cg + s * 32);
@@ -586,7 +594,11 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
     const bool gv = g < g1;                                      // warp-uniform
     const double* cgc = coef + ((size_t)g * S) * 32 + lane;   // this group's A fragments
     double a[SA];
-    if (!STREAM_A && gv) {
+    if (kScanNoPrefetch && !STREAM_A && gv) {
+      // this group's operands, loaded before the turn barrier: the L2 round trip overlaps the wait
+#pragma unroll
+      for (int s = 0; s < SA; ++s) a[s] = __ldg(cgc + s * 32);
+    } else if (!STREAM_A && gv) {
 #pragma unroll
       for (int s = 0; s < SA; ++s) a[s] = an[s];
       if (g + kCtaWarps < g1) {                                // prefetch the next group's operands
@@ -634,6 +646,7 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
           }
 #pragma unroll
           for (int s = 0; s < SE; ++s) {
+            if (s == kScanHandoff) bar_arrive(2 - wg);          // early hand-off (tuning)
             const double ae = STREAM_A ? __ldg(cgc + s * 32) : a[STREAM_A ? 0 : s];
 #pragma unroll
             for (int t = 0; t < NA; ++t) {
@@ -656,7 +669,8 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
           }
         }
       }
-      bar_arrive(2 - wg);                       // hand the pipe to the other group
+      if (!(gv && MIRROR && kScanCFold && kScanHandoff >= 0 && kScanHandoff < SE))
+        bar_arrive(2 - wg);                     // hand the pipe to the other group
       if (!gv) continue;
       flush_cand(pcand, cap, cidx, cf);                // the previous epilogue's deferred candidate
       if (!MIRROR) {
