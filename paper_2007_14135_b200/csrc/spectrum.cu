@@ -517,10 +517,17 @@ __device__ __forceinline__ void scan_epilogue(long long (&v)[2 * NA], int lane, 
     hit &= hit - 1;
     const int pos = R * q + j, i = base + pos;
     if (pos < 1 || pos > W - 2 || i < ilo || i > ihi) continue;   // halo / grid ends (Q9)
-    long long f = 0;
+    long long f;                                           // v[j]: select tree on the bits of j
+    {
+      long long t[R / 2];
 #pragma unroll
-    for (int jj = 0; jj < R; ++jj)
-      if (jj == j) f = v[jj];
+      for (int k = 0; k < R / 2; ++k) t[k] = (j & 1) ? v[2 * k + 1] : v[2 * k];
+#pragma unroll
+      for (int w = R / 4, bit = 2; w >= 1; w /= 2, bit *= 2)
+#pragma unroll
+        for (int k = 0; k < w; ++k) t[k] = (j & bit) ? t[2 * k + 1] : t[2 * k];
+      f = t[0];
+    }
     if (pc.slot < 0) {                                     // deferred: stored at the next flush
       pc.slot = atomicAdd(cnt + b, 1);
       pc.b = b;
