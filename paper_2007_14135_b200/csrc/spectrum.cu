@@ -724,11 +724,23 @@ cudaError_t launch_scan_cta(const doa_plan_s* p, int64_t B, float* P, cudaStream
   const int64_t gx = (nwb + NB - 1) / NB;                        // angle columns
   const int64_t ngroups = (B + 7) / 8;
   const int64_t slots = (int64_t)sm_count() * occ;
-  // frame chunk: ~4 waves of resident CTAs, >= 64 groups (8 per warp) per CTA
-  int64_t per = (gx * ngroups) / (DOA_SCAN_WAVES * slots);
-  if (per < 64) per = 64;
-  if (per > ngroups) per = ngroups;
-  const int64_t gy = (ngroups + per - 1) / per;
+  // frame chunks.  Large batches: ~4 waves of resident CTAs with >= 64 groups (8 per warp) per CTA.
+  // Small batches (fewer than 4 waves' worth of 256-group CTAs): k whole waves (gx * gy <= k *
+  // slots) of CTAs with >= 256 groups each, so the per-CTA steering table stays amortised (B = 8192
+  // at c4: one wave of 512-group CTAs, 0.202 -> 0.183 ms per launch; profiles/scan_ab_r02x.txt).
+  const int64_t kw = (gx * ngroups) / (slots * 256);
+  int64_t per, gy;
+  if (kw >= DOA_SCAN_WAVES) {
+    per = (gx * ngroups) / (DOA_SCAN_WAVES * slots);
+    if (per < 64) per = 64;
+    if (per > ngroups) per = ngroups;
+    gy = (ngroups + per - 1) / per;
+  } else {
+    gy = ((kw < 1 ? 1 : kw) * slots) / gx;
+    if (gy < 1) gy = 1;
+    if (gy > ngroups) gy = ngroups;
+    per = (ngroups + gy - 1) / gy;
+  }
   const dim3 grid((unsigned)gx, (unsigned)gy);
   const bool sym = p->sym != 0;
   count_launch();
