@@ -234,79 +234,123 @@ __global__ void peaks2d_kernel(const double* __restrict__ fbuf, int64_t B, int64
 
 // The same 2-D findPeaks on tiles: a CTA takes TA consecutive azimuth rows of one frame (all nel
 // elevations) plus the two neighbouring rows (wrapped when the azimuth wraps), stages them in shared
-// memory once, and tests every core point against its 8 neighbours there — f is read ~(TA+2)/TA
-// times instead of up to 9 times through L1/L2.  Same rule, same candidates (their list order may
-// differ; doa_peaks sorts).  Used when (TA+2) * nel fits the tile (nel <= kPk2MaxNel).
+// memory once — (TA+2) x (nel+2) values, a sentinel column on each side and sentinel halo rows
+// where no neighbour exists (no wrap at the grid edge, or naz == 1, whose wrapped rows are the
+// point's own row) — and tests every core point against its 8 neighbours there without branches.
+// Raster order decides strictness: a neighbour that precedes the point must be strictly larger
+// (fp < n), one that follows may be equal (fp <= n).  The row above precedes the point unless it is
+// the wrapped last row; the row below follows it unless it is the wrapped first row; within a row
+// the left neighbour precedes, the right one follows.  f is floored, so never NaN; the sentinel is
+// a NaN and the tests are the unordered ones (!(fp >= n), !(fp > n)), so a missing neighbour never
+// blocks a peak — the rule of peaks2d_kernel.  Same candidates (their list order may differ;
+// doa_peaks sorts).  Staging: one warp per tile row (the row's source is warp-uniform), 8-byte
+// asynchronous copies (LDGSTS) so a thread's loads are all in flight at once; rows shorter than a
+// warp use a flat element walk.  Used when (TA+2) * (nel+2) fits the tile (nel <= kPk2MaxNel).
 constexpr int kPk2Vals = 2048;       // core values per tile (TA = kPk2Vals / nel rows)
 constexpr int kPk2MaxNel = 2048;
+constexpr int kPkRows = 4;           // core rows per sliding-window work item
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
 __global__ void __launch_bounds__(256) peaks2d_tile_kernel(const double* __restrict__ fbuf, int64_t naz, int64_t nel,
                                                            int TA, int wrap, int cap, int32_t* __restrict__ cnt,
                                                            int32_t* __restrict__ cidx, double* __restrict__ cf,
                                                            float* __restrict__ P) {
-  extern __shared__ double ft[];                       // [TA + 2][nel]: rows ia0-1 .. ia0+TA
-  __shared__ int rowok[2];                             // halo rows present (wrap or inside the grid)
+  extern __shared__ double ft[];                       // [TA + 2][nel + 2]: rows ia0-1 .. ia0+TA
   const int64_t L = naz * nel;
   const int64_t b = blockIdx.y;
-  const int64_t ia0 = (int64_t)blockIdx.x * TA;
-  const int nr = (int)(ia0 + TA <= naz ? TA : naz - ia0);   // core rows of this tile
+  const int nazI = (int)naz, nelI = (int)nel, W = nelI + 2;
+  const int ia0 = (int)blockIdx.x * TA;
+  const int nr = ia0 + TA <= nazI ? TA : nazI - ia0;   // core rows of this tile
   const double* fb = fbuf + (size_t)b * L;
-  {                                                    // stage rows ia0-1 .. ia0+nr (int32 walk, no divisions)
-    const int nelI = (int)nel, nvals = (nr + 2) * nelI;
-    const int sr = (int)(blockDim.x / nelI), se = (int)(blockDim.x - sr * nelI);
-    int row = (int)(threadIdx.x / nelI), ie = (int)(threadIdx.x - (threadIdx.x / nelI) * nelI);
-    for (int e = threadIdx.x; e < nvals; e += blockDim.x, row += sr, ie += se) {
-      if (ie >= nelI) { ie -= nelI; ++row; }
-      int64_t ja = ia0 - 1 + row;
-      bool ok = ja >= 0 && ja < naz;
-      if (!ok && wrap) { ja = ja < 0 ? ja + naz : ja - naz; ok = true; }
-      ft[e] = ok ? __ldcs(fb + ja * nel + ie) : 0.0;      // f is read once: streaming load
-    }
-  }
-  if (threadIdx.x < 2) {
-    const int64_t ja = threadIdx.x == 0 ? ia0 - 1 : ia0 + nr;
-    rowok[threadIdx.x] = (ja >= 0 && ja < naz) || wrap;
-  }
-  __syncthreads();
-  // Core points: thread -> (row, elevation) advanced incrementally (no divisions); neighbour tests on
-  // the IEEE bits (f is floored, so positive and never NaN: the bits order like the values).  Raster
-  // order decides strictness: the row above precedes the point (strict) unless it is the wrapped
-  // last row, the row below follows it (non-strict) unless it is the wrapped first row; within the
-  // row the left neighbour precedes, the right one follows.  With naz == 1 the wrapped rows are the
-  // point's own row, whose tests repeat the in-row ones, so they are skipped.
-  const int nelI = (int)nel;
-  const long long* fi = reinterpret_cast<const long long*>(ft);
-  const bool up_ok = rowok[0] && naz > 1, dn_ok = rowok[1] && naz > 1;
-  const int steps_r = (int)(blockDim.x / nelI), steps_e = (int)(blockDim.x - steps_r * nelI);
-  int r = 1 + (int)(threadIdx.x / nelI), ie = (int)(threadIdx.x - (threadIdx.x / nelI) * nelI);
-  for (; r <= nr; r += steps_r, ie += steps_e) {
-    if (ie >= nelI) { ie -= nelI; ++r; if (r > nr) break; }
-    const int64_t ia = ia0 + r - 1;
-    const int c = r * nelI + ie;
-    const long long fp = fi[c];
-    const bool lft = ie > 0, rgt = ie < nelI - 1;
-    // same row: left strict, right non-strict
-    bool peak = (!lft || fp < fi[c - 1]) && (!rgt || fp <= fi[c + 1]);
-    const bool up = (r > 1) || up_ok, dn = (r < nr) || dn_ok;
-    if (up) {                                            // row ia - 1 (wrapped: the last row, after p)
-      const bool st = ia > 0;
-      const int u = c - nelI;
-      const long long a = fi[u], l = lft ? fi[u - 1] : 0, g = rgt ? fi[u + 1] : 0;
-      peak = peak && (st ? fp < a : fp <= a) && (!lft || (st ? fp < l : fp <= l)) && (!rgt || (st ? fp < g : fp <= g));
-    }
-    if (dn) {                                            // row ia + 1 (wrapped: the first row, before p)
-      const bool st = ia == naz - 1;
-      const int d = c + nelI;
-      const long long a = fi[d], l = lft ? fi[d - 1] : 0, g = rgt ? fi[d + 1] : 0;
-      peak = peak && (st ? fp < a : fp <= a) && (!lft || (st ? fp < l : fp <= l)) && (!rgt || (st ? fp < g : fp <= g));
-    }
-    const int64_t pidx = ia * nel + ie;
-    if (P) P[(size_t)b * L + pidx] = to_p32a(__longlong_as_double(fp));
-    if (peak) {
-      const int slot = atomicAdd(cnt + b, 1);
-      if (slot < cap) {
-        cidx[(size_t)b * cap + slot] = (int32_t)pidx;
-        cf[(size_t)b * cap + slot] = __longlong_as_double(fp);
+  const double kSent = __longlong_as_double(0x7FF8000000000000LL);   // quiet NaN
+  auto src_row = [&](int r) {                          // source row of tile row r (-1: sentinel row)
+    const int ja = ia0 - 1 + r;
+    if (ja >= 0 && ja < nazI) return ja;
+    if (!wrap || nazI == 1) return -1;
+    return ja < 0 ? nazI - 1 : 0;
+  };
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  if (nelI >= 32) {
+    for (int r = warp; r < nr + 2; r += nwarps) {
+      const int ja = src_row(r);
+      double* dst = ft + r * W;
+      if (lane == 0) { dst[0] = kSent; dst[nelI + 1] = kSent; }
+      if (ja < 0) {
+        for (int c = lane; c < nelI; c += 32) dst[1 + c] = kSent;
+      } else {
+        const double* src = fb + (size_t)ja * nelI;
+        for (int c = lane; c < nelI; c += 32) cp_async8(dst + 1 + c, src + c);
       }
+    }
+  } else {
+    const int nvals = (nr + 2) * W;
+    const int sr = (int)(blockDim.x / W), se = (int)(blockDim.x - sr * W);
+    int r = (int)(threadIdx.x / W), c = (int)(threadIdx.x - r * W);
+    for (int e = threadIdx.x; e < nvals; e += blockDim.x, r += sr, c += se) {
+      if (c >= W) { c -= W; ++r; }
+      const int ja = src_row(r);
+      if (ja < 0 || c == 0 || c > nelI) ft[e] = kSent;
+      else cp_async8(ft + e, fb + (size_t)ja * nelI + (c - 1));
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  // Tests: work item = (chunk of kPkRows core rows, elevation column); a thread slides a 3 x 3
+  // window down its column, so each point costs 3 shared loads instead of 9 (the tile is bound by
+  // shared-memory bandwidth), and consecutive lanes take consecutive columns (conflict-free).
+  const int nchunks = (nr + kPkRows - 1) / kPkRows;
+  const int items = nchunks * nelI;
+  const int sc = (int)(blockDim.x / nelI), se = (int)(blockDim.x - sc * nelI);
+  int ch = (int)(threadIdx.x / nelI), ie = (int)(threadIdx.x - ch * nelI);
+  for (int it = threadIdx.x; it < items; it += blockDim.x, ch += sc, ie += se) {
+    if (ie >= nelI) { ie -= nelI; ++ch; }
+    const int r0 = ch * kPkRows;                         // first core row of the chunk
+    const double* col = ft + r0 * W + ie;                // tile row r0 = the row above core row r0
+    double a0 = col[0], a1 = col[1], a2 = col[2];
+    double b0 = col[W], b1 = col[W + 1], b2 = col[W + 2];
+#pragma unroll
+    for (int k = 0; k < kPkRows; ++k) {
+      if (r0 + k >= nr) break;
+      const double* cr = col + (k + 2) * W;
+      const double c0 = cr[0], c1 = cr[1], c2 = cr[2];
+      const int ia = ia0 + r0 + k;
+      const double fp = b1;
+      // unordered tests (ltu: fp < n, leu: fp <= n; both true for the NaN sentinel)
+      bool peak;
+      if (ia != 0 && ia != nazI - 1) {                   // interior row: above precedes, below follows
+        unsigned pk;
+        asm("{\n\t.reg .pred p;\n\t"
+            "setp.ltu.f64 p, %1, %2;\n\t"
+            "setp.ltu.and.f64 p, %1, %3, p;\n\t"
+            "setp.ltu.and.f64 p, %1, %4, p;\n\t"
+            "setp.ltu.and.f64 p, %1, %5, p;\n\t"
+            "setp.leu.and.f64 p, %1, %6, p;\n\t"
+            "setp.leu.and.f64 p, %1, %7, p;\n\t"
+            "setp.leu.and.f64 p, %1, %8, p;\n\t"
+            "setp.leu.and.f64 p, %1, %9, p;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(pk)
+            : "d"(fp), "d"(a0), "d"(a1), "d"(a2), "d"(b0), "d"(b2), "d"(c0), "d"(c1), "d"(c2));
+        peak = pk != 0;
+      } else {                                           // first / last row: wrapped neighbours' order
+        const bool upf = ia == 0, dnf = ia != nazI - 1;  // row above follows p / row below follows p
+        const bool pu = upf ? (!(fp > a0) & !(fp > a1) & !(fp > a2)) : (!(fp >= a0) & !(fp >= a1) & !(fp >= a2));
+        const bool pd = dnf ? (!(fp > c0) & !(fp > c1) & !(fp > c2)) : (!(fp >= c0) & !(fp >= c1) & !(fp >= c2));
+        peak = pu & pd & !(fp >= b0) & !(fp > b2);
+      }
+      const int64_t pidx = (int64_t)ia * nel + ie;
+      if (P) P[(size_t)b * L + pidx] = to_p32a(fp);
+      if (peak) {
+        const int slot = atomicAdd(cnt + b, 1);
+        if (slot < cap) {
+          cidx[(size_t)b * cap + slot] = (int32_t)pidx;
+          cf[(size_t)b * cap + slot] = fp;
+        }
+      }
+      a0 = b0; a1 = b1; a2 = b2;
+      b0 = c0; b1 = c1; b2 = c2;
     }
   }
 }
@@ -349,7 +393,7 @@ cudaError_t launch_array_spectrum(const doa_plan_s* p, const double* lam, const 
   count_launch();
   if (p->nel <= kPk2MaxNel && B < 65536) {
     const int TA = (int)(kPk2Vals / p->nel < 1 ? 1 : kPk2Vals / p->nel);
-    const size_t smem = (size_t)(TA + 2) * p->nel * sizeof(double);
+    const size_t smem = (size_t)(TA + 2) * (p->nel + 2) * sizeof(double);
     kernel_occupancy(peaks2d_tile_kernel, 256, smem);                  // sets the smem attribute (> 48 KB)
     const dim3 grid((unsigned)((p->naz + TA - 1) / TA), (unsigned)B);
     peaks2d_tile_kernel<<<grid, 256, smem, s>>>(p->fbuf, p->naz, p->nel, TA, p->wrap, p->cap, p->cnt, p->cand_idx,
