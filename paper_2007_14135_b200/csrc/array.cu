@@ -127,22 +127,6 @@ struct ArrShape {
 };
 constexpr int kArrWarps = 8;
 
-// table entry j of flattened grid point pt
-__device__ __forceinline__ double arr_entry(int j, int K, int64_t pt, const double* __restrict__ dpos, double az0,
-                                            double daz, double el0, double del, int64_t nel) {
-  if (j == 0) return 1.0;
-  if (j >= K) return 0.0;
-  const int64_t ia = pt / nel, ie = pt - (pt / nel) * nel;
-  const double az = __dadd_rn(__dmul_rn((double)ia, daz), az0);
-  const double el = __dadd_rn(__dmul_rn((double)ie, del), el0);
-  double saz, caz, sel, cel;
-  sincospi(az / 180.0, &saz, &caz);
-  sincospi(el / 180.0, &sel, &cel);
-  const int pr = (j - 1) >> 1;
-  const double arg = 2.0 * (dpos[3 * pr] * saz * sel + dpos[3 * pr + 1] * caz * sel + dpos[3 * pr + 2] * cel);
-  return (j & 1) ? cospi(arg) : sinpi(arg);       // z_pq = exp(j pi arg): (cos, sin) at j = (odd, even)
-}
-
 template <int M>
 __global__ void __launch_bounds__(kArrWarps * 32) scan_array_kernel(const double* __restrict__ coef, int64_t B,
                                                                    int64_t per, const double* __restrict__ dpos,
@@ -154,11 +138,32 @@ __global__ void __launch_bounds__(kArrWarps * 32) scan_array_kernel(const double
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q = lane & 3, r = lane >> 2;
   const int64_t col0 = (int64_t)blockIdx.x * NB * W;
+  // the column's direction sines / cosines once per angle (Eq. 2), then one cospi / sinpi per entry
+  __shared__ double dir[NB * W][4];                                // sin az, cos az, sin el, cos el
+  for (int a = threadIdx.x; a < NB * W; a += kArrWarps * 32) {
+    const int64_t pt = col0 + a;
+    if (pt < L) {
+      const int64_t ia = pt / nel, ie = pt - (pt / nel) * nel;
+      const double az = __dadd_rn(__dmul_rn((double)ia, daz), az0);
+      const double el = __dadd_rn(__dmul_rn((double)ie, del), el0);
+      sincospi(az / 180.0, &dir[a][0], &dir[a][1]);
+      sincospi(el / 180.0, &dir[a][2], &dir[a][3]);
+    }
+  }
+  __syncthreads();
   for (int e = threadIdx.x; e < NB * S * NA * 32; e += kArrWarps * 32) {
     const int ln = e & 31, t = (e >> 5) % NA, s = (e / (32 * NA)) % S, k = e / (32 * NA * S);
-    const int64_t pt = col0 + (int64_t)k * W + 8 * t + (ln >> 2);
+    const int a = k * W + 8 * t + (ln >> 2);
+    const int64_t pt = col0 + a;
     const int j = 4 * s + (ln & 3);
-    Ta[e] = (pt < L) ? arr_entry(j, K, pt, dpos, az0, daz, el0, del, nel) : (j == 0 ? 1.0 : 0.0);
+    double v = j == 0 ? 1.0 : 0.0;
+    if (pt < L && j > 0 && j < K) {   // z_pq = exp(j pi arg): (cos, sin) at j = (odd, even), Eq. 2
+      const double saz = dir[a][0], caz = dir[a][1], sel = dir[a][2], cel = dir[a][3];
+      const int pr = (j - 1) >> 1;
+      const double arg = 2.0 * (dpos[3 * pr] * saz * sel + dpos[3 * pr + 1] * caz * sel + dpos[3 * pr + 2] * cel);
+      v = (j & 1) ? cospi(arg) : sinpi(arg);
+    }
+    Ta[e] = v;
   }
   __syncthreads();
   const int64_t ngroups = (B + 7) / 8;
@@ -248,7 +253,7 @@ __global__ void peaks2d_kernel(const double* __restrict__ fbuf, int64_t B, int64
 // warp use a flat element walk.  Used when (TA+2) * (nel+2) fits the tile (nel <= kPk2MaxNel).
 constexpr int kPk2Vals = 2048;       // core values per tile (TA = kPk2Vals / nel rows)
 constexpr int kPk2MaxNel = 2048;
-constexpr int kPkRows = 4;           // core rows per sliding-window work item
+constexpr int kPkRows = 11;           // core rows per sliding-window work item
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
