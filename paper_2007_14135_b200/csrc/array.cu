@@ -126,21 +126,6 @@ struct ArrShape {
   static constexpr int NB = 2;
 };
 constexpr int kArrWarps = 8;
-#ifndef DOA_ARR_AREG
-#define DOA_ARR_AREG 0
-#endif
-#ifndef DOA_ARR_PP
-#define DOA_ARR_PP 0
-#endif
-__device__ __forceinline__ void arr_bar_sync(int id) {
-  if (id == 1) asm volatile("bar.sync 1, 256;\n" ::: "memory");
-  else asm volatile("bar.sync 2, 256;\n" ::: "memory");
-}
-__device__ __forceinline__ void arr_bar_arrive(int id) {
-  if (id == 1) asm volatile("bar.arrive 1, 256;\n" ::: "memory");
-  else asm volatile("bar.arrive 2, 256;\n" ::: "memory");
-}
-
 template <int M>
 __global__ void __launch_bounds__(kArrWarps * 32) scan_array_kernel(const double* __restrict__ coef, int64_t B,
                                                                    int64_t per, const double* __restrict__ dpos,
@@ -183,59 +168,40 @@ __global__ void __launch_bounds__(kArrWarps * 32) scan_array_kernel(const double
   const int64_t ngroups = (B + 7) / 8;
   const int64_t g0 = (int64_t)blockIdx.y * per;
   const int64_t g1 = (g0 + per < ngroups) ? g0 + per : ngroups;
-#if DOA_ARR_PP
-  // ping-pong of the DMMA pipe between the CTA's two warp groups (as scan_cta_kernel): CTA-uniform
-  // trip counts, warps past the chunk's last group still take their turns
-  const int wg = warp >> 2;
-  const int64_t nit = (g1 - g0 + kArrWarps - 1) / kArrWarps;
-  if (wg == 1) arr_bar_arrive(1);
-  for (int64_t it = 0; it < nit; ++it) {
-    const int64_t g = g0 + warp + it * kArrWarps;
-    const bool gv = g < g1;
-#else
   for (int64_t g = g0 + warp; g < g1; g += kArrWarps) {
-    constexpr bool gv = true;
-#endif
     const double* cg = coef + ((size_t)g * S) * 32 + lane;
     const int64_t b = g * 8 + r;
-#if DOA_ARR_AREG
-    double areg[S];                                                 // the group's A fragments, both blocks
-    if (gv) {
+    // M <= 8 (S <= 16): the group's A fragments in registers, loaded once for both blocks (e1 360x90
+    // x 4096: 1.014 -> 0.982 ms per plan); larger M streams them from L1 per k-step (registers)
+    constexpr bool AREG = S <= 16;
+    double areg[AREG ? S : 1];
+    if (AREG) {
 #pragma unroll
-      for (int s = 0; s < S; ++s) areg[s] = __ldg(cg + s * 32);
+      for (int s = 0; s < (AREG ? S : 1); ++s) areg[s] = __ldg(cg + s * 32);
     }
-#endif
 #pragma unroll 1
     for (int k = 0; k < NB; ++k) {
       const int64_t base = col0 + (int64_t)k * W;
-      if (base >= L) break;                                         // CTA-uniform
+      if (base >= L) break;
       const double* Tk = Ta + (size_t)k * S * NA * 32 + lane;
       double acc[NA][2];
 #pragma unroll
       for (int t = 0; t < NA; ++t) { acc[t][0] = 0.0; acc[t][1] = 0.0; }
-#if DOA_ARR_PP
-      arr_bar_sync(1 + wg);
-#endif
-      if (gv) {
-#if DOA_ARR_AREG
+      if constexpr (AREG) {
 #pragma unroll
-#else
-#pragma unroll 4
-#endif
         for (int s = 0; s < S; ++s) {
-#if DOA_ARR_AREG
-          const double a = areg[s];
-#else
+#pragma unroll
+          for (int t = 0; t < NA; ++t) dmma_a(acc[t][0], acc[t][1], areg[s], Tk[(s * NA + t) * 32]);
+        }
+      } else {
+#pragma unroll 4
+        for (int s = 0; s < S; ++s) {
           const double a = __ldg(cg + s * 32);
-#endif
 #pragma unroll
           for (int t = 0; t < NA; ++t) dmma_a(acc[t][0], acc[t][1], a, Tk[(s * NA + t) * 32]);
         }
       }
-#if DOA_ARR_PP
-      arr_bar_arrive(2 - wg);
-#endif
-      if (gv && b < B) {
+      if (b < B) {
 #pragma unroll
         for (int t = 0; t < NA; ++t)
 #pragma unroll
@@ -247,9 +213,6 @@ __global__ void __launch_bounds__(kArrWarps * 32) scan_array_kernel(const double
       }
     }
   }
-#if DOA_ARR_PP
-  if (wg == 0) arr_bar_sync(1);                                     // the other group's last hand-off
-#endif
 }
 
 // 2-D findPeaks (G2) on the floored f: thread per (frame, grid point).
