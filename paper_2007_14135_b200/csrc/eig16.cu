@@ -47,6 +47,10 @@ __device__ constexpr int kBlockOrder[28] = {14, 11, 10, 16, 13, 8, 25, 15, 4, 6,
 // that cost a third of the rotation-parameter instructions.  The rotation code feeds them
 // unguarded values (a zero pivot gives inf/NaN intermediates) and selects the identity rotation
 // at the end, keeping selects off the latency chain.
+#ifndef DOA_EIG_NEWTON2
+#define DOA_EIG_NEWTON2 0
+#endif
+#if DOA_EIG_NEWTON2
 __device__ __forceinline__ double rsqrt_pos(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -62,6 +66,23 @@ __device__ __forceinline__ double rcp_pos(double x) {
   y = y * fma(-x, y, 2.0);
   return y;
 }
+#else
+// One third-order correction instead of two Newton steps: with e = 1 - x y0^2 (the seed's relative
+// error is ~2^-22, so e^3 ~ 2^-66 is below an ulp) y = y0 (1 + e/2 + 3e^2/8): four dependent
+// FP64 operations instead of six on the rotation-parameter chain; rcp likewise y0 (1 + e + e^2).
+__device__ __forceinline__ double rsqrt_pos(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-(x * y), y, 1.0);
+  return fma(y * e, fma(e, 0.375, 0.5), y);
+}
+__device__ __forceinline__ double rcp_pos(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x, y, 1.0);
+  return fma(y, fma(e, e, e), y);
+}
+#endif
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
