@@ -389,16 +389,18 @@ __global__ void __launch_bounds__(kCoefBigWarps * 32) coef_big_kernel(const doub
 //     Ts[k][s][t][lane] = T_{4s + lane%4}(angle base_k + 8t + lane/4)
 // (fp64 sincospi, no recurrence) so every B-fragment load is one conflict-free 8-byte LDS.
 // The CTA's 8 warps stream disjoint 8-frame groups of the chunk (warp w: g0+w, g0+w+8, ...):
-// one coalesced A-fragment load per k-step (prefetched one group ahead, reused for all blocks),
+// one coalesced A-fragment load per k-step (issued before the group's turn barrier, reused for
+// all blocks),
 // S x NA DMMAs per block (8 independent accumulator chains), then the fused epilogue:
 //   D fragment: lane holds frame lane/4, block positions 16(lane%4) + 0..15.
 //   floor (Q12) + peak test (Q9/Q10) in the INTEGER domain — for positive doubles the IEEE bits
 //   order like the values, so the FP64 pipe stays with the DMMAs; 17 compares per 16 angles in
-//   registers, two shuffles for the run ends; rare atomic append to the frame's candidate list;
-//   optional fp32 P.
+//   registers, two shuffles for the run ends; atomic append to the frame's candidate list (the
+//   value picked by a select tree on the run index); optional fp32 P.
 // MIRROR (symmetric grids, Q26): the blocks cover only the lower half i <= H = ceil(L/2) (one
-// angle past the middle as the last neighbour); the even and odd k-steps accumulate separately,
-// E and O, and the tile yields f_i = E + O and f_{L-1-i} = E - O (psi_{L-1-i} = -psi_i exactly):
+// angle past the middle as the last neighbour); the odd k-steps accumulate O, the even ones E on
+// top of it (O is the first E DMMA's C operand), and the tile yields f_i = E + O straight from the
+// tensor pipe and f_{L-1-i} = E - O = f_i - 2 O by one DFMA (psi_{L-1-i} = -psi_i exactly):
 // half the DMMAs and half the steering table per grid angle.  In the mirrored half the grid index
 // runs backwards through the tile, so the peak test's strict/non-strict sides swap.
 // Grid: blockIdx.x = angle column, blockIdx.y = frame chunk (~4 waves of resident CTAs).
@@ -410,18 +412,6 @@ constexpr int kScanNA = 8;        // 8-angle tiles per block (a lane owns 2*NA c
 #define DOA_SCAN_MINB 2
 #endif
 constexpr int kScanMinBlocks = DOA_SCAN_MINB; // __launch_bounds__ min blocks per SM
-#ifndef DOA_SCAN_CFOLD
-#define DOA_SCAN_CFOLD 1
-#endif
-constexpr bool kScanCFold = DOA_SCAN_CFOLD != 0;
-#ifndef DOA_SCAN_NOPF
-#define DOA_SCAN_NOPF 1
-#endif
-constexpr bool kScanNoPrefetch = DOA_SCAN_NOPF != 0;
-#ifndef DOA_SCAN_HANDOFF
-#define DOA_SCAN_HANDOFF -1
-#endif
-constexpr int kScanHandoff = DOA_SCAN_HANDOFF;   // E k-step at which the pipe is handed over (-1: end)
 #ifndef DOA_SCAN_WAVES
 #define DOA_SCAN_WAVES 4
 #endif
@@ -580,12 +570,6 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
   __syncthreads();
   const int64_t g0 = y * per;
   const int64_t g1 = (g0 + per < ngroups) ? g0 + per : ngroups;
-  double an[SA];
-  if (!kScanNoPrefetch && !STREAM_A && g0 + warp < g1) {
-    const double* cg = coef + ((size_t)(g0 + warp) * S) * 32 + lane;
-#pragma unroll
-    for (int s = 0; s < SA; ++s) an[s] = __ldg(cg + s * 32);
-  }
   // Ping-pong: warps 0-3 and 4-7 take turns on the DMMA pipe — a warp group issues
   // its block's DMMAs, hands the pipe to the other group (named barriers 1/2) and runs its
   // epilogue while the other group's DMMAs execute, so the pipe never idles on an epilogue phase
@@ -601,18 +585,11 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
     const bool gv = g < g1;                                      // warp-uniform
     const double* cgc = coef + ((size_t)g * S) * 32 + lane;   // this group's A fragments
     double a[SA];
-    if (kScanNoPrefetch && !STREAM_A && gv) {
+    if (!STREAM_A && gv) {
       // this group's operands, loaded before the turn barrier: the L2 round trip overlaps the wait
+      // (a one-group-ahead prefetch held 16 more registers and was 2.5% slower)
 #pragma unroll
       for (int s = 0; s < SA; ++s) a[s] = __ldg(cgc + s * 32);
-    } else if (!STREAM_A && gv) {
-#pragma unroll
-      for (int s = 0; s < SA; ++s) a[s] = an[s];
-      if (g + kCtaWarps < g1) {                                // prefetch the next group's operands
-        const double* cg = coef + ((size_t)(g + kCtaWarps) * S) * 32 + lane;
-#pragma unroll
-        for (int s = 0; s < SA; ++s) an[s] = __ldg(cg + s * 32);
-      }
     }
     const int b = (int)(g * 8) + r;
     const bool frame_ok = gv && b < B;
@@ -634,17 +611,13 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
 #pragma unroll
           for (int s = 0; s < S; ++s) {
             const double av = STREAM_A ? __ldg(cgc + s * 32) : a[STREAM_A ? 0 : s];
-            if (!MIRROR || s < SE) {
 #pragma unroll
-              for (int t = 0; t < NA; ++t) dmma_884(acc[t][0], acc[t][1], av, Tk[(s * NA + t) * 32]);
-            } else {
-#pragma unroll
-              for (int t = 0; t < (MIRROR ? NA : 1); ++t) dmma_884(aco[t][0], aco[t][1], av, Tk[(s * NA + t) * 32]);
-            }
+            for (int t = 0; t < NA; ++t) dmma_884(acc[t][0], acc[t][1], av, Tk[(s * NA + t) * 32]);
           }
-        } else if (kScanCFold) {
+        } else {
           // O chains first, then the E chains accumulate onto O: acc = E + O = f_i directly, and
-          // f_{L-1-i} = E - O = acc - 2 O takes one DFMA per element (instead of two DADDs)
+          // f_{L-1-i} = E - O = acc - 2 O takes one DFMA per element (two separate chains combined
+          // with two DADDs per element were 6% slower: the DADDs share the FP64 datapath)
 #pragma unroll
           for (int s = 0; SE + s < S; ++s) {
             const double ao = STREAM_A ? __ldg(cgc + (SE + s) * 32) : a[STREAM_A ? 0 : SE + s];
@@ -653,7 +626,6 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
           }
 #pragma unroll
           for (int s = 0; s < SE; ++s) {
-            if (s == kScanHandoff) bar_arrive(2 - wg);          // early hand-off (tuning)
             const double ae = STREAM_A ? __ldg(cgc + s * 32) : a[STREAM_A ? 0 : s];
 #pragma unroll
             for (int t = 0; t < NA; ++t) {
@@ -661,23 +633,9 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
               else dmma_884(acc[t][0], acc[t][1], ae, Tk[(s * NA + t) * 32]);
             }
           }
-        } else {
-          // E and O k-steps interleaved: 2 NA independent accumulator chains per step pair
-#pragma unroll
-          for (int s = 0; s < SE; ++s) {
-            const double ae = STREAM_A ? __ldg(cgc + s * 32) : a[STREAM_A ? 0 : s];
-            const bool has_o = SE + s < S;
-            const double ao = has_o ? (STREAM_A ? __ldg(cgc + (SE + s) * 32) : a[STREAM_A ? 0 : (SE + s < S ? SE + s : 0)]) : 0.0;
-#pragma unroll
-            for (int t = 0; t < NA; ++t) {
-              dmma_884(acc[t][0], acc[t][1], ae, Tk[(s * NA + t) * 32]);
-              if (has_o) dmma_884(aco[MIRROR ? t : 0][0], aco[MIRROR ? t : 0][1], ao, Tk[((SE + s) * NA + t) * 32]);
-            }
-          }
         }
       }
-      if (!(gv && MIRROR && kScanCFold && kScanHandoff >= 0 && kScanHandoff < SE))
-        bar_arrive(2 - wg);                     // hand the pipe to the other group
+      bar_arrive(2 - wg);                       // hand the pipe to the other group
       if (!gv) continue;
       flush_cand(pcand, cap, cidx, cf);                // the previous epilogue's deferred candidate
       if (!MIRROR) {
@@ -695,13 +653,8 @@ __global__ void __launch_bounds__(kCtaWarps * 32, kScanMinBlocks) scan_cta_kerne
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const double ev = acc[t][e], od = aco[MIRROR ? t : 0][e];
-            if (kScanCFold) {
-              fl[2 * t + e] = __double_as_longlong(ev);                  // f_i       = (O + E)
-              fh[2 * t + e] = __double_as_longlong(fma(-2.0, od, ev));   // f_{L-1-i} = f_i - 2 O
-            } else {
-              fl[2 * t + e] = __double_as_longlong(ev + od);      // f_i          = E + O
-              fh[2 * t + e] = __double_as_longlong(ev - od);      // f_{L-1-i}    = E - O
-            }
+            fl[2 * t + e] = __double_as_longlong(ev);                    // f_i       = (O + E)
+            fh[2 * t + e] = __double_as_longlong(fma(-2.0, od, ev));     // f_{L-1-i} = f_i - 2 O
           }
         scan_epilogue<NA, WRITE_P, false>(fl, lane, base, 1, H - 1, H - 1, L, b, frame_ok, cap, cnt, cidx, cf, P, pcand);
         scan_epilogue<NA, WRITE_P, true>(fh, lane, base, 1, L - 1 - H, L - 1 - H, L, b, frame_ok, cap, cnt, cidx, cf, P, pcand);
