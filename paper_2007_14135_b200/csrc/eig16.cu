@@ -445,11 +445,12 @@ __global__ void __launch_bounds__(kHWarps * 32, DOA_EIGH_MINB) eig16h_kernel(con
         const double irh = rsqrt_pos(h2);
         const double hh = h2 * irh;
         const double q = fabs(d) + hh;
-        const double uu = 0.5 * q * irh;
-        const double sabs = rr * rsqrt_pos(2.0 * hh * q);
+        const double uu = 0.5 * q * irh;                 // c^2
+        const double iu = rsqrt_pos(uu);                 // 2 hh q = 4 h2 uu: s = r / sqrt(2 hh q) = r irh iu / 2
+        const double sabs = (0.5 * rr * irh) * iu;
         const double trabs = r2 * rcp_pos(q);
         const double tr = rot ? (d < 0.0 ? -trabs : trabs) : 0.0;
-        Pc[hl] = make_double2(rot ? uu * rsqrt_pos(uu) : 1.0, rot ? (d < 0.0 ? -sabs : sabs) : 0.0);
+        Pc[hl] = make_double2(rot ? uu * iu : 1.0, rot ? (d < 0.0 ? -sabs : sabs) : 0.0);
         Pe[hl] = make_double2(rot ? axy.x * ir : 1.0, rot ? -axy.y * ir : 0.0);
         *diagp<N>(An, px) = axx - tr;
         *diagp<N>(An, py) = ayy + tr;
@@ -538,12 +539,13 @@ __device__ __forceinline__ RotP rot_params_s(double axx, double ayy, double2 axy
   const double irh = rsqrt_pos(h2);
   const double hh = h2 * irh;
   const double q = fabs(d) + hh;
-  const double uu = 0.5 * q * irh;
-  const double sabs = rr * rsqrt_pos(2.0 * hh * q);
+  const double uu = 0.5 * q * irh;                       // c^2 (same operations as eig16h)
+  const double iu = rsqrt_pos(uu);
+  const double sabs = (0.5 * rr * irh) * iu;
   const double trabs = r2 * rcp_pos(q);
   RotP p;
   p.tr = rot ? (d < 0.0 ? -trabs : trabs) : 0.0;
-  p.c = rot ? uu * rsqrt_pos(uu) : 1.0;
+  p.c = rot ? uu * iu : 1.0;
   p.s = rot ? (d < 0.0 ? -sabs : sabs) : 0.0;
   p.er = rot ? axy.x * ir : 1.0;
   p.ei = rot ? -axy.y * ir : 0.0;
