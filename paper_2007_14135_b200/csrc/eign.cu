@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(EigN<N>::T, 1) eigN_kernel(const double2* __re
         // Short-chain parameters (same rotation as GvL sym.schur2): with d = (a_yy - a_xx)/2,
         // r = |a_xy|, h = sqrt(d^2 + r^2), q = |d| + h:  t = sign(d) r / q,  c = sqrt(q / 2h),
         // s = sign(d) r / sqrt(2 h q)  (c^2 + s^2 = 1 exactly in exact arithmetic), t r = sign(d) r^2 / q.
-        // c's critical path is two MUFU+Newton reciprocal square roots instead of four chained
+        // c's critical path is two MUFU+correction reciprocal square roots instead of four chained
         // reciprocal (square) roots; s, e and t r run on parallel branches.  The MUFU inputs are not
         // guarded (a zero pivot gives inf/NaN intermediates): the identity is selected at the end,
         // keeping selects off the chain.
@@ -202,11 +202,12 @@ __global__ void __launch_bounds__(EigN<N>::T, 1) eigN_kernel(const double2* __re
         const double h = h2 * irh;
         const double q = fabs(d) + h;
         const double u = 0.5 * q * irh;                       // c^2, in [1/2, 1]
-        const double sabs = rr * rsqrt_p(2.0 * h * q);
+        const double iu = rsqrt_p(u);                         // 2 h q = 4 h2 c^2: s = r irh iu / 2
+        const double sabs = (0.5 * rr * irh) * iu;
         const double trabs = r2 * rcp_p(q);
         const double tr = rot ? (d < 0.0 ? -trabs : trabs) : 0.0;   // t |a_xy|
         PrmN p;
-        p.c = rot ? u * rsqrt_p(u) : 1.0;
+        p.c = rot ? u * iu : 1.0;
         p.s = rot ? (d < 0.0 ? -sabs : sabs) : 0.0;
         p.er = rot ? axy.x * ir : 1.0;
         p.ei = rot ? -axy.y * ir : 0.0;
