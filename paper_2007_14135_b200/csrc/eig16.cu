@@ -43,33 +43,13 @@ __device__ constexpr int kBlockOrder[28] = {14, 11, 10, 16, 13, 8, 25, 15, 4, 6,
 
 
 // Branch-free reciprocal (square root) for positive normal arguments: MUFU seed (rsqrt/rcp
-// .approx.ftz.f64) + two Newton steps, ~1 ulp.  The library versions add special-case branches
-// that cost a third of the rotation-parameter instructions.  The rotation code feeds them
-// unguarded values (a zero pivot gives inf/NaN intermediates) and selects the identity rotation
-// at the end, keeping selects off the latency chain.
-#ifndef DOA_EIG_NEWTON2
-#define DOA_EIG_NEWTON2 0
-#endif
-#if DOA_EIG_NEWTON2
-__device__ __forceinline__ double rsqrt_pos(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double hx = 0.5 * x;
-  y = y * fma(-hx * y, y, 1.5);
-  y = y * fma(-hx * y, y, 1.5);
-  return y;
-}
-__device__ __forceinline__ double rcp_pos(double x) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  y = y * fma(-x, y, 2.0);
-  y = y * fma(-x, y, 2.0);
-  return y;
-}
-#else
-// One third-order correction instead of two Newton steps: with e = 1 - x y0^2 (the seed's relative
-// error is ~2^-22, so e^3 ~ 2^-66 is below an ulp) y = y0 (1 + e/2 + 3e^2/8): four dependent
-// FP64 operations instead of six on the rotation-parameter chain; rcp likewise y0 (1 + e + e^2).
+// .approx.ftz.f64) + one third-order correction, within 1 ulp (tools/rsqrt_check.cu,
+// tests/test_gpu_rsqrt.py).  The library versions add special-case branches that cost a third of
+// the rotation-parameter instructions.  The rotation code feeds them unguarded values (a zero
+// pivot gives inf/NaN intermediates) and selects the identity rotation at the end, keeping selects
+// off the latency chain.  With e = 1 - x y0^2 (the seed's relative error is below 2^-20, measured
+// 9.2e-7, so (5/16) e^3 < 2^-61) y = y0 (1 + e/2 + 3e^2/8): four dependent FP64 operations instead
+// of the six of two Newton steps on the rotation-parameter chain; rcp likewise y0 (1 + e + e^2).
 __device__ __forceinline__ double rsqrt_pos(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -82,7 +62,6 @@ __device__ __forceinline__ double rcp_pos(double x) {
   const double e = fma(-x, y, 1.0);
   return fma(y, fma(e, e, e), y);
 }
-#endif
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
